@@ -1,0 +1,317 @@
+/*
+ * pswim_c.h — C-ABI drop-in boundary of the B200-native MRS / rod / Parareal hot path.
+ *
+ * Every entry point replaces one reference interface of arxiv/paper_2604_12083's CPU
+ * library `pintswim` (paths relative to /root/reference/proj).  Plain pointers and sizes
+ * only: no torch, no C++ types.  Layout conventions follow the reference exactly:
+ *
+ *   Vec3            3 doubles, AoS                         (include/pintswim/geom.hpp:10-18)
+ *   Mat3 / Rot3     9 doubles, row-major                   (include/pintswim/geom.hpp:37-40)
+ *   packed state    per node 12 doubles [x, d1, d2, d3],   (src/io.cpp:10-25, io.hpp:14-17)
+ *                   rods concatenated in order
+ *
+ * Errors: every call returns 0 (PSWIM_OK) or a PSWIM_E* code; pswim_last_error() gives text.
+ * Device-side failures (non-finite loads, stiffness guard, degenerate segment) are raised
+ * through a device flag and reported by the first call that synchronises the context
+ * (pswim_sync, every *_host entry point, pswim_propagate).
+ *
+ * Device pointers ("d_" prefix) must be cudaMalloc'd memory of the context's device.
+ * Host pointers ("h_" prefix) are ordinary (or pinned) host memory.
+ */
+#ifndef PSWIM_C_H
+#define PSWIM_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes ------------------------------------------------------------------ */
+enum {
+    PSWIM_OK = 0,
+    PSWIM_EINVAL = 1,            /* std::invalid_argument in the reference               */
+    PSWIM_EUNSUPPORTED_WALL = 2, /* stokes.cpp:15-17 image_wall throws runtime_error     */
+    PSWIM_ENONFINITE = 3,        /* stokes.cpp:21-25 non-finite load entry                */
+    PSWIM_ESTIFF = 4,            /* propagators.hpp:24-26 StiffnessError                 */
+    PSWIM_EDEGENERATE = 5,       /* rod.cpp:53-55 degenerate segment                      */
+    PSWIM_ECUDA = 6,             /* CUDA runtime failure                                  */
+    PSWIM_ECOMM = 7,             /* transport (NCCL / peer copy / callback) failure       */
+    PSWIM_ESTATE = 8             /* std::logic_error in the reference                    */
+};
+
+/* ---- parameter blocks ---------------------------------------------------------------- */
+/* KernelParams, include/pintswim/stokes.hpp:13-17.  wall_mode: 0 free_space, 1 image_wall. */
+typedef struct pswim_kernel_params {
+    double epsilon;
+    double mu;
+    int32_t wall_mode;
+    int32_t _pad;
+} pswim_kernel_params;
+
+/* ScenarioConfig, include/pintswim/scenario.hpp:16-35.  epsilon = 0 / lj_sigma = 0 mean
+ * "derive the default" exactly as make_scenario (scenario.cpp:10-29).
+ * placement: 0 grid, 1 random. */
+typedef struct pswim_scenario {
+    int64_t rod_count;
+    int64_t nodes_per_rod;
+    double rod_length;
+    double a1, a2, a3;          /* MaterialParams bending, bending, torsion  (rod.hpp:28-31) */
+    double b1, b2, b3;          /* shear, shear, stretch                                      */
+    double amplitude;           /* WaveformParams A, f, lambda               (rod.hpp:34-39) */
+    double frequency;
+    double wavelength;
+    double epsilon;
+    double mu;
+    int32_t wall_mode;
+    int32_t placement;
+    double lj_well_depth;
+    double lj_sigma;
+    double wall_clearance;
+    uint64_t seed;
+    double fine_dt;
+    double horizon;
+} pswim_scenario;
+
+/* Fills the reference defaults of ScenarioConfig (scenario.hpp:16-35). */
+void pswim_scenario_defaults(pswim_scenario* sc);
+
+/* Scenario (scenario.hpp:38-44) after make_scenario: derived ds, epsilon, sigma, window. */
+typedef struct pswim_resolved {
+    double ds;
+    double epsilon;
+    double mu;
+    double lj_sigma;
+    double lj_cutoff;
+    int64_t lj_self_exclusion;
+    int64_t total_nodes;
+} pswim_resolved;
+
+/* make_scenario, src/scenario.cpp:10-29 (validation + derivation). */
+int pswim_scenario_resolve(const pswim_scenario* sc, pswim_resolved* out);
+
+/* build_initial_state + pack_state, src/scenario.cpp:71-120 and src/io.cpp:10-25.
+ * h_state must hold 12 * rod_count * nodes_per_rod doubles. */
+int pswim_build_initial_state(const pswim_scenario* sc, double* h_state);
+
+/* ---- context ------------------------------------------------------------------------- */
+typedef struct pswim_ctx pswim_ctx;
+
+/* Creates a context on `device` with its own non-blocking stream (priority 0 = default,
+ * <0 = higher priority as cudaStreamCreateWithPriority).  `sc` may be NULL for an
+ * MRS-only context (pswim_mrs_velocities / pswim_sqrt_rotation_batched).
+ * Replaces the implicit global state of the reference (OpenMP team + timing atomics,
+ * src/propagators.cpp:11-36); one context per device stream, not shared across threads
+ * without external synchronisation. */
+pswim_ctx* pswim_create(int device, const pswim_scenario* sc, int stream_priority);
+void pswim_destroy(pswim_ctx* ctx);
+const char* pswim_last_error(const pswim_ctx* ctx);
+void* pswim_stream(pswim_ctx* ctx);            /* cudaStream_t of the context             */
+int pswim_sync(pswim_ctx* ctx);                /* stream sync + device error-flag check   */
+int pswim_device(const pswim_ctx* ctx);
+
+/* ---- MRS operator -------------------------------------------------------------------- */
+/* evaluate_velocities, include/pintswim/stokes.hpp:43-44 / src/stokes.cpp:76-95.
+ * u_i = (1/mu) sum_j [f_j H1 + (f_j.r) r H2 + (n_j x r) H3], omega likewise, r = t_i - s_j,
+ * all targets x all sources, self term included.  Deterministic: fixed launch geometry and
+ * fixed-order split-source reduction, bitwise reproducible run to run.
+ * Stream-ordered on the context stream, no host sync inside.  ENONFINITE (non-finite f/n)
+ * is reported at the next sync. */
+int pswim_mrs_velocities(pswim_ctx* ctx, const double* d_targets, int64_t n_targets,
+                         const double* d_sources, const double* d_f, const double* d_n,
+                         int64_t n_sources, const pswim_kernel_params* kp, double* d_u,
+                         double* d_omega);
+
+/* Same operator through host buffers (H2D copies, kernel, D2H copies, sync, error check). */
+int pswim_mrs_velocities_host(pswim_ctx* ctx, const double* h_targets, int64_t n_targets,
+                              const double* h_sources, const double* h_f, const double* h_n,
+                              int64_t n_sources, const pswim_kernel_params* kp, double* h_u,
+                              double* h_omega);
+
+/* h_functions, src/stokes.cpp:59-74 (device evaluation, batched). */
+int pswim_h_functions(pswim_ctx* ctx, const double* d_r, int64_t count, double epsilon,
+                      double* d_h5 /* count x 5 */);
+
+/* ---- rotation square root ------------------------------------------------------------ */
+/* sqrt_rotation, include/pintswim/rotation.hpp:34 / src/rotation.cpp:91-107, batched:
+ * `count` row-major 3x3 rotations in, their half-angle square roots out. */
+int pswim_sqrt_rotation_batched(pswim_ctx* ctx, const double* d_r9, int64_t count, double* d_s9);
+int pswim_sqrt_rotation_host(pswim_ctx* ctx, const double* h_r9, int64_t count, double* h_s9);
+
+/* ---- rod mechanics ------------------------------------------------------------------- */
+/* internal_loads + nodal_loads, src/rod.cpp:36-109, over every rod of the context's
+ * scenario.  d_state: packed state.  Outputs per node (N = total nodes) f, n as N x 3;
+ * optional d_seg_force / d_seg_moment (rods x (M-1) x 3) receive the segment loads. */
+int pswim_rod_loads(pswim_ctx* ctx, const double* d_state, double t, double* d_f, double* d_n,
+                    double* d_seg_force, double* d_seg_moment);
+
+/* lj_repulsion, src/rod.cpp:124-174 (raw pair forces, N x 3, before the 1/ds factor). */
+int pswim_lj_forces(pswim_ctx* ctx, const double* d_state, double* d_forces);
+
+/* ---- propagators --------------------------------------------------------------------- */
+enum { PSWIM_EULER = 0, PSWIM_RK2 = 1 };
+
+/* rhs, src/propagators.cpp:38-91.  d_extra_f / d_extra_n (N x 3) may be NULL. */
+int pswim_rhs(pswim_ctx* ctx, const double* d_state, double t, const double* d_extra_f,
+              const double* d_extra_n, double* d_u, double* d_omega);
+
+/* advance_state, src/propagators.cpp:93-124 (Euler position update, exact Rodrigues triad
+ * rotation, stiffness guard, reorthonormalize).  d_out may not alias d_state. */
+int pswim_advance_state(pswim_ctx* ctx, const double* d_state, const double* d_u,
+                        const double* d_omega, double dt, double* d_out);
+
+/* step_euler / step_rk2, src/propagators.cpp:126-133. */
+int pswim_step(pswim_ctx* ctx, int scheme, const double* d_state, double t, double dt,
+               double* d_out);
+
+/* propagate, src/propagators.cpp:135-162.  steps_per_interval > 0 overrides dt exactly as
+ * StepperConfig (propagators.hpp:15-20); otherwise (t1-t0)/dt must be integral to 1e-9.
+ * t accumulates as t += dt (propagators.cpp:157-160).  d_in and d_out may alias.
+ * Synchronises the context (returns ESTIFF / EDEGENERATE / ENONFINITE). */
+int pswim_propagate(pswim_ctx* ctx, const double* d_in, double t0, double t1, int scheme,
+                    int64_t steps_per_interval, double dt, double* d_out);
+
+/* Host-buffer propagate (e2e boundary: H2D, propagate, D2H). */
+int pswim_propagate_host(pswim_ctx* ctx, const double* h_in, double t0, double t1, int scheme,
+                         int64_t steps_per_interval, double dt, double* h_out);
+
+/* Stage timers, propagators.hpp:55-65 (CUDA events: initialization = load assembly,
+ * velocity = MRS, triad_update = advance).  Seconds, accumulated since the last reset. */
+typedef struct pswim_timing {
+    double initialization;
+    double velocity;
+    double triad_update;
+} pswim_timing;
+void pswim_timing_enable(pswim_ctx* ctx, int on);
+void pswim_timing_reset(pswim_ctx* ctx);
+pswim_timing pswim_timing_snapshot(pswim_ctx* ctx);
+
+/* ---- metric / corrector -------------------------------------------------------------- */
+/* rod_position_metric, src/io.cpp:49-68 (denominator from the FIRST argument). */
+int pswim_position_metric(pswim_ctx* ctx, const double* d_x, const double* d_y, int64_t len,
+                          double* h_result);
+
+/* corrected, src/parareal.cpp:47-54: out = (x_prime + g_new) - g_old, elementwise. */
+int pswim_parareal_correct(pswim_ctx* ctx, const double* d_x_prime, const double* d_g_new,
+                           const double* d_g_old, int64_t len, double* d_out);
+
+/* ---- Parareal ------------------------------------------------------------------------ */
+/* ParallelPlan, include/pintswim/parareal.hpp:30-45.  mode: 0 regular, 1 pipelined. */
+typedef struct pswim_plan {
+    double t0;
+    double horizon;
+    int32_t intervals;
+    int32_t workers;
+    double cost_ratio;
+    int32_t max_iterations;
+    int32_t mode;
+    double tolerance;
+} pswim_plan;
+
+/* ConvergenceReport, parareal.hpp:47-52.  Arrays sized by the caller (>= intervals). */
+typedef struct pswim_report {
+    double* eta_tilde;
+    double* eta;          /* may be NULL */
+    int32_t iterations_used;
+    int32_t converged;
+    int32_t eta_count;
+    int32_t _pad;
+    double wall_seconds;
+    double schedule_idle; /* W, schedule_trace.cpp:43-49 */
+} pswim_report;
+
+/* Propagator hook, the C form of parareal::PropagatorFn (parareal.hpp:19):
+ * out = F(t0, t1, in).  `stream` is the CUDA stream (or NULL for host propagators) the
+ * call must be ordered on; buffers live where the driver's memory kind says. */
+typedef int (*pswim_propagator_fn)(void* user, double t0, double t1, const double* in,
+                                   double* out, int64_t len, void* stream);
+
+/* Trace event (schedule_trace.hpp:14-19).  kind: 0 coarse, 1 fine, 2 correct, 3 idle. */
+typedef struct pswim_trace_event {
+    int32_t worker;
+    int32_t kind;
+    double t_start;
+    double t_end;
+} pswim_trace_event;
+
+/* parareal::run (parareal.hpp:85-86, src/parareal.cpp:118-438) over HOST states with
+ * caller-supplied host propagators: the physics-agnostic engine (regular / pipelined task
+ * graph, worker lanes, stop rule, trace).  metric: point_dim-wise pointwise metric
+ * (parareal.cpp:15-34) with point stride `metric_stride` (12 and dim 3 = rod positions,
+ * io.cpp:49-68; stride = dim = d for pointwise_metric(d)).
+ * states_out: (intervals+1) x len.  trace_out may be NULL; trace_cap bounds it and
+ * *trace_len receives the number of events. */
+int pswim_parareal_run_host(const pswim_plan* plan, pswim_propagator_fn coarse, void* coarse_user,
+                            pswim_propagator_fn fine, void* fine_user, const double* h_x0,
+                            int64_t len, int32_t metric_dim, int32_t metric_stride,
+                            const double* h_reference /* (n+1) x len or NULL */,
+                            double* h_states_out, pswim_report* report,
+                            pswim_trace_event* trace_out, int64_t trace_cap, int64_t* trace_len);
+
+/* parareal::run with GPU propagators: coarse = Euler(coarse_steps), fine = RK2(fine_steps)
+ * as harness::prepare (src/harness.cpp:5-33).  Each engine worker owns one device context
+ * (stream) on `device`; states stay in HBM.  h_x0 / h_states_out / h_reference are host. */
+int pswim_parareal_run_gpu(const pswim_plan* plan, const pswim_scenario* sc, int device,
+                           int64_t fine_steps, int64_t coarse_steps, const double* h_x0,
+                           const double* h_reference, double* h_states_out, pswim_report* report,
+                           pswim_trace_event* trace_out, int64_t trace_cap, int64_t* trace_len);
+
+/* ---- time-sliced Parareal across ranks (one slice per GPU) ---------------------------- */
+/* Transport between slice ranks.  Buffers are device pointers for GPU transports, host
+ * pointers for host transports.  All calls are ordered on `stream` (NULL for host). */
+typedef struct pswim_transport {
+    void* user;
+    int32_t rank;
+    int32_t world;
+    int (*send)(void* user, const double* buf, int64_t len, int32_t peer, void* stream);
+    int (*recv)(void* user, double* buf, int64_t len, int32_t peer, void* stream);
+    /* in-place elementwise max over ranks of `len` doubles */
+    int (*allreduce_max)(void* user, double* buf, int64_t len, void* stream);
+} pswim_transport;
+
+/* Rank driver: rank p owns interval p+1 of a plan with intervals == world.  Runs the
+ * pipelined (or regular) Parareal recurrence of src/parareal.cpp:58-89 with one state
+ * hand-off per iteration to rank p+1 and one allreduce(max) of the iteration metric.
+ * Final boundary state X[k_final][p+1] goes to h_state_out; the report is identical on
+ * every rank.  GPU form: fine = RK2, coarse = Euler on the context's device. */
+int pswim_parareal_rank_gpu(const pswim_plan* plan, const pswim_scenario* sc, pswim_ctx* ctx,
+                            const pswim_transport* tr, int64_t fine_steps, int64_t coarse_steps,
+                            const double* h_x0, const double* h_reference_slice /* or NULL */,
+                            double* h_state_out, pswim_report* report);
+
+/* Host form of the same rank driver (host propagators + host transport): used by the
+ * world_size>1 CPU tests of the rank logic. */
+int pswim_parareal_rank_host(const pswim_plan* plan, pswim_propagator_fn coarse, void* coarse_user,
+                             pswim_propagator_fn fine, void* fine_user, const pswim_transport* tr,
+                             const double* h_x0, int64_t len, int32_t metric_dim,
+                             int32_t metric_stride, const double* h_reference_slice,
+                             double* h_state_out, pswim_report* report);
+
+/* NCCL transport for one process per GPU.  The unique id (128 bytes) is produced by rank 0
+ * with pswim_nccl_unique_id and distributed by the caller (e.g. torch.distributed store). */
+int pswim_nccl_unique_id(uint8_t* id128);
+pswim_transport* pswim_nccl_transport_create(const uint8_t* id128, int32_t rank, int32_t world,
+                                             int device);
+void pswim_nccl_transport_destroy(pswim_transport* tr);
+
+/* In-process transport: `world` slice ranks as threads of one process, each on its own
+ * context (any device mix), hand-offs by stream-ordered peer copies + events. */
+int pswim_parareal_run_threads(const pswim_plan* plan, const pswim_scenario* sc,
+                               const int* devices /* world entries */, int64_t fine_steps,
+                               int64_t coarse_steps, const double* h_x0,
+                               const double* h_reference, double* h_states_out,
+                               pswim_report* report);
+
+/* ---- microbenchmarks used by bench.py for the roofline denominators ------------------- */
+/* Measured FP64 FMA throughput (FLOP/s, 2 per DFMA) of a register-resident DFMA loop over
+ * the whole chip on the context's device; ms = kernel time. */
+int pswim_dfma_peak(pswim_ctx* ctx, double* flops_per_s, double* ms);
+
+/* Library version string. */
+const char* pswim_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSWIM_C_H */
