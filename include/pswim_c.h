@@ -275,7 +275,7 @@ typedef struct pswim_transport {
  * hand-off per iteration to rank p+1 and one allreduce(max) of the iteration metric.
  * Final boundary state X[k_final][p+1] goes to h_state_out; the report is identical on
  * every rank.  GPU form: fine = RK2, coarse = Euler on the context's device. */
-int pswim_parareal_rank_gpu(const pswim_plan* plan, const pswim_scenario* sc, pswim_ctx* ctx,
+int pswim_parareal_rank_gpu(const pswim_plan* plan, const pswim_scenario* sc, int device,
                             const pswim_transport* tr, int64_t fine_steps, int64_t coarse_steps,
                             const double* h_x0, const double* h_reference_slice /* or NULL */,
                             double* h_state_out, pswim_report* report);

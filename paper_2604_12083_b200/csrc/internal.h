@@ -1,0 +1,68 @@
+// internal.h — declarations shared between the translation units of libpswim.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/pswim_c.h"
+
+namespace pswim {
+
+// Device error flag bits (OR-ed by kernels, read at sync).
+enum : unsigned {
+    kFlagNonFinite = 1u << 0,   // -> PSWIM_ENONFINITE
+    kFlagStiff = 1u << 1,       // -> PSWIM_ESTIFF
+    kFlagDegenerate = 1u << 2,  // -> PSWIM_EDEGENERATE
+    kFlagAxis = 1u << 3,        // -> PSWIM_EINVAL (from_axis_angle axis check)
+};
+
+// ---- MRS (mrs.cu) ----------------------------------------------------------------------
+struct MrsPlan {
+    int64_t nt = 0, ns = 0;
+    int target_blocks = 0;  // ceil(nt / kMrsTargets)
+    int chunks = 0;         // source chunks (grid.y)
+    size_t scratch_doubles = 0;
+    size_t counters = 0;
+};
+constexpr int kMrsThreads = 256;  // one target per thread
+MrsPlan mrs_plan(int64_t nt, int64_t ns);
+// Launches the all-pairs kernel (+ fused fixed-order split-source reduction).
+// d_scratch >= plan.scratch_doubles, d_counters >= plan.counters (zeroed once; the kernel
+// leaves them zero again).
+cudaError_t mrs_launch(const MrsPlan& plan, const double* tgt, const double* src, const double* f,
+                       const double* n, double eps, double mu, double* u, double* w, double* scratch,
+                       unsigned* counters, unsigned* flags, cudaStream_t st);
+cudaError_t h_functions_launch(const double* r, int64_t count, double eps, double* h5, cudaStream_t st);
+
+// ---- rod / propagator kernels (rod.cu) --------------------------------------------------
+struct RodParams {
+    int64_t rods = 0, m = 0;
+    double length = 1.0, ds = 0.0, inv_ds = 0.0;
+    double a[3] = {0, 0, 0}, b[3] = {0, 0, 0};
+    double amplitude = 0.0, frequency = 0.0, wavelength = 1.0;
+    double epsilon = 0.0, mu = 1.0;
+    double lj_well = 0.0, lj_sigma = 0.0, lj_cutoff = 0.0;
+    int64_t lj_excl = 4;
+};
+// internal + nodal loads: state (packed 12/node) -> pos, f, n (N x 3); optional segment
+// loads; extra loads added after LJ as rhs does (propagators.cpp:70-84).
+cudaError_t rod_loads_launch(const RodParams& p, const double* state, double t, double* pos, double* f,
+                             double* n, double* seg_f, double* seg_n, const double* lj, const double* extra_f,
+                             const double* extra_n, unsigned* flags, cudaStream_t st);
+cudaError_t lj_launch(const RodParams& p, const double* state, double* forces, cudaStream_t st);
+cudaError_t advance_launch(const RodParams& p, const double* state, const double* u, const double* w, double dt,
+                           double* out, unsigned* flags, cudaStream_t st);
+cudaError_t sqrt_batched_launch(const double* r9, int64_t count, double* s9, cudaStream_t st);
+cudaError_t metric_launch(const double* x, const double* y, int64_t len, double* d_partial, int* d_count,
+                          double* d_result, cudaStream_t st);
+cudaError_t correct_launch(const double* xp, const double* gn, const double* go, int64_t len, double* out,
+                           cudaStream_t st);
+cudaError_t dfma_launch(double* sink, int blocks, int iters, cudaStream_t st);
+
+// ---- host scenario (scenario.cpp) -------------------------------------------------------
+int resolve_scenario(const pswim_scenario* sc, pswim_resolved* out, std::string* err);
+RodParams rod_params(const pswim_scenario* sc, const pswim_resolved& rs);
+
+}  // namespace pswim

@@ -1,0 +1,131 @@
+"""GPU parity of rhs / advance_state / step / propagate (reference propagators.cpp:38-162)."""
+import numpy as np
+import pytest
+
+from helpers import rel_field_err
+
+pytestmark = pytest.mark.gpu
+
+
+def scen(**kw):
+    from paper_2604_12083_b200.scenario import ScenarioConfig, make_scenario
+
+    return make_scenario(ScenarioConfig(**kw))
+
+
+CASES = [dict(rod_count=1, nodes_per_rod=21), dict(rod_count=1, nodes_per_rod=100),
+         dict(rod_count=4, nodes_per_rod=21, placement=1, lj_well_depth=0.01, seed=2),
+         dict(rod_count=9, nodes_per_rod=64, epsilon=0.08)]
+
+
+@pytest.mark.parametrize("kw", CASES)
+def test_rhs_matches_oracle(gpu, oracle, kw):
+    from paper_2604_12083_b200.propagators import rhs
+    from paper_2604_12083_b200.scenario import build_initial_state
+    from oracle.pyoracle import Scenario as OS
+
+    sc = scen(**kw)
+    x = build_initial_state(sc)
+    osc = OS.make(**kw)
+    assert np.array_equal(x, oracle.build_initial_state(osc))
+    # perturb so every term is active
+    rng = np.random.default_rng(1)
+    y = x.reshape(-1, 12).copy()
+    y[:, 0:3] += rng.normal(scale=1e-3, size=(len(y), 3))
+    y = y.reshape(-1)
+    got = rhs(y, 0.137, sc)
+    want = oracle.rhs(osc, y, 0.137)
+    assert rel_field_err((got.u, got.omega), want) < 1e-10
+
+
+def test_rhs_extra_loads_linear(gpu, oracle):
+    from paper_2604_12083_b200.propagators import rhs
+    from paper_2604_12083_b200.scenario import build_initial_state
+    from paper_2604_12083_b200.stokes import LoadSet
+    from oracle.pyoracle import Scenario as OS
+
+    sc = scen(rod_count=1, nodes_per_rod=21)
+    x = build_initial_state(sc)
+    rng = np.random.default_rng(5)
+    ef, en = rng.uniform(-1, 1, (21, 3)), rng.uniform(-1, 1, (21, 3))
+    got = rhs(x, 0.1, sc, LoadSet(ef, en))
+    want = oracle.rhs(OS.make(rod_count=1, nodes_per_rod=21), x, 0.1, ef.reshape(-1), en.reshape(-1))
+    assert rel_field_err((got.u, got.omega), want) < 1e-10
+
+
+def test_advance_matches_oracle_and_stiffness(gpu, oracle):
+    from paper_2604_12083_b200.propagators import StiffnessError, SystemVelocities, advance_state
+    from paper_2604_12083_b200.scenario import build_initial_state
+    from oracle.pyoracle import Scenario as OS
+
+    sc = scen(rod_count=2, nodes_per_rod=33)
+    x = build_initial_state(sc)
+    rng = np.random.default_rng(3)
+    u = rng.uniform(-0.1, 0.1, (66, 3))
+    w = rng.uniform(-2, 2, (66, 3))
+    w[5] = 0.0
+    got = advance_state(x, SystemVelocities(u, w), 0.01, sc)
+    want = oracle.advance_state(OS.make(rod_count=2, nodes_per_rod=33), x, u, w, 0.01)
+    assert np.max(np.abs(got - want)) < 1e-14
+    with pytest.raises(StiffnessError):
+        advance_state(x, SystemVelocities(np.ones((66, 3)), w), 1.0, sc)
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_propagate_matches_oracle(gpu, oracle, scheme):
+    """1 x 100 flagellum (BASELINE config 1), 200 steps at dt=1e-5."""
+    from paper_2604_12083_b200.propagators import StepperConfig, propagate
+    from paper_2604_12083_b200.scenario import build_initial_state
+    from oracle.pyoracle import Scenario as OS
+
+    kw = dict(rod_count=1, nodes_per_rod=100)
+    sc = scen(**kw)
+    x = build_initial_state(sc)
+    got = propagate(x, 0.0, 2e-3, StepperConfig(0.0, scheme, 200), sc)
+    want = oracle.propagate(OS.make(**kw), x, 0.0, 2e-3, scheme, steps=200)
+    assert oracle.position_metric(want, got) < 1e-10
+    moved = oracle.position_metric(x, want)
+    assert moved > 1e-6
+
+
+def test_propagate_64x256_short(gpu, oracle):
+    """BASELINE config 3 suspension (64 x 256, eps=0.08): 3 RK2 steps vs the oracle."""
+    import torch
+    from paper_2604_12083_b200.propagators import StepperConfig, propagate
+    from paper_2604_12083_b200.scenario import build_initial_state
+    from oracle.pyoracle import Scenario as OS
+
+    kw = dict(rod_count=64, nodes_per_rod=256, epsilon=0.08)
+    sc = scen(**kw)
+    x = build_initial_state(sc)
+    got = propagate(torch.as_tensor(x, device=gpu), 0.0, 3e-6, StepperConfig(1e-6, 1, 0), sc).cpu().numpy()
+    want = oracle.propagate(OS.make(**kw), x, 0.0, 3e-6, 1, steps=0, dt=1e-6, threads=8)
+    assert oracle.position_metric(want, got) < 1e-10
+
+
+def test_propagate_bitwise_deterministic_and_composes(gpu):
+    from paper_2604_12083_b200.propagators import StepperConfig, propagate
+    from paper_2604_12083_b200.scenario import build_initial_state
+
+    sc = scen(rod_count=1, nodes_per_rod=21)
+    x = build_initial_state(sc)
+    a = propagate(x, 0.0, 0.0625, StepperConfig(0.0, 1, 8), sc)
+    b = propagate(x, 0.0, 0.0625, StepperConfig(0.0, 1, 8), sc)
+    assert np.array_equal(a, b)
+    half = StepperConfig(0.0, 1, 4)
+    two = propagate(propagate(x, 0.0, 0.03125, half, sc), 0.03125, 0.0625, half, sc)
+    assert np.array_equal(two, a)
+    assert np.array_equal(propagate(x, 0.3, 0.3, StepperConfig(0.0, 1, 8), sc), x)
+    from paper_2604_12083_b200 import InvalidArgument
+
+    with pytest.raises(InvalidArgument):
+        propagate(x, 0.0, 0.1, StepperConfig(0.013, 0, 0), sc)
+
+
+def test_quiet_rod_zero_rhs(gpu):
+    from paper_2604_12083_b200.propagators import rhs
+    from paper_2604_12083_b200.scenario import ScenarioConfig, WaveformParams, build_initial_state, make_scenario
+
+    sc = make_scenario(ScenarioConfig(rod_count=1, nodes_per_rod=21, waveform=WaveformParams(0.0, 2 * np.pi, 1.0)))
+    v = rhs(build_initial_state(sc), 0.0, sc)
+    assert np.abs(v.u).max() < 1e-13 and np.abs(v.omega).max() < 1e-13
