@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""bench.py — MRS Gpair-interactions/s (+ simulated RK2 time-steps/s) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One JSON line on rank 0:
+
+* value        MRS all-pairs evaluation, BASELINE.json configs[1] (N = 16384 regularized
+               points, targets = sources, eps = 0.1, mu = 1, inputs ~ U[-0.5,0.5)^3), inputs
+               resident in HBM, L2 flushed (256 MiB write) before every timed step, each step
+               timed with CUDA events on the launching stream; whole-job Gpair/s = N_gpus *
+               N^2 / max-over-ranks step time (weak scaling: every rank evaluates its own
+               suspension, no data-path collective).
+* e2e          the same evaluation through the C-ABI host entry point
+               (pswim_mrs_velocities_host): pinned host buffers, H2D + kernel + D2H + sync
+               inside the timed region.
+* roofline     dominant kernel (mrs_kernel): 103 FLOP/pair (stokes.cpp:29-55 as
+               written) x N^2 / average launch time, against the FP64 DFMA peak measured
+               live in this run (MEASURED_PEAKS.json has no FP64 entry).
+* time_steps   secondary metric: simulated RK2 time-steps/s.  N=1: serial fine RK2 on
+               configs[2] (64 x 256 suspension, eps = 0.08, dt = 1e-6).  N>1: pipelined
+               Parareal, one time slice per GPU over NCCL (configs[3]).
+* cpu_baseline the reference's own evaluate_velocities (oracle/_ref, OpenMP, all host
+               threads) on a bounded target sample of the same workload (rank 0, N=1).
+
+``--impl reference`` times that reference CPU path alone (rank 0; other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_POINTS = 16384
+EPS, MU = 0.1, 1.0
+FLOP_PER_PAIR = 103
+WORKLOAD = "MRS all-pairs velocity evaluation, N=16384 regularized points (BASELINE configs[1])"
+
+
+def synthetic_inputs(n: int, seed: int):
+    """x, f, n i.i.d. U[-0.5, 0.5)^3 drawn per point in that order (bench_kernels.cpp:46-63
+    with numpy's generator instead of mt19937_64)."""
+    rng = np.random.default_rng(seed)
+    u = rng.random((n, 3, 3)) - 0.5
+    return [np.ascontiguousarray(u[:, i, :]) for i in range(3)]
+
+
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) == 7:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        smax = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def reduce_max(value: float, device=None) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier():
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
+# ------------------------------------------------------------------------------------------
+def cpu_reference_mrs(n_targets: int, reps: int, threads: int | None = None):
+    """The reference's evaluate_velocities (OpenMP) on n_targets x N_POINTS pairs."""
+    from oracle.pyoracle import Oracle
+
+    ref = Oracle("ref")
+    if threads:
+        ref.set_threads_(threads)
+    cores = ref.max_threads_()
+    x, f, tq = synthetic_inputs(N_POINTS, 7)
+    tgt = np.ascontiguousarray(x[:n_targets])
+    ref.evaluate_velocities(tgt[:64], x, f, tq, EPS, MU, parallel=True)  # OpenMP team warm-up
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        ref.evaluate_velocities(tgt, x, f, tq, EPS, MU, parallel=True)
+        times.append(time.perf_counter() - t0)
+    return times, cores
+
+
+def run_reference_arm(args) -> None:
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    n_targets = args.ref_targets
+    times, cores = cpu_reference_mrs(n_targets, args.steps + args.warmup)
+    t = times[args.warmup:] or times
+    per = sum(t) / len(t)
+    value = n_targets * N_POINTS / per / 1e9
+    sample = f"{n_targets} targets x {N_POINTS} sources per step (bounded sample of the N=16384 all-pairs workload)"
+    line = {
+        "impl": "reference", "metric": "MRS Gpair-interactions/s", "value": value, "unit": "Gpair/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * per,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "points": N_POINTS, "epsilon": EPS, "mu": MU, "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": value, "unit": "Gpair/s", "cores": cores, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "Gpair/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_2604_12083_b200 import _lib
+    from paper_2604_12083_b200.device import Context, dptr
+
+    L = _lib.lib()
+    ctx = Context(local)
+    st = ctx.torch_stream()
+    kp = _lib.KernelParams(EPS, MU, 0, 0)
+    n = N_POINTS
+
+    # --- measured FP64 peak (roofline denominator) ---
+    dfma_peak, _ = ctx.dfma_peak()
+
+    # --- device-resident inputs ---
+    x, f, tq = synthetic_inputs(n, 7 + rank)
+    dx, df, dn = (torch.as_tensor(a, device=dev) for a in (x, f, tq))
+    du = torch.empty_like(dx)
+    dw = torch.empty_like(dx)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def launch():
+        ctx.check(L.pswim_mrs_velocities(ctx.handle, dptr(dx), n, dptr(dx), dptr(df), dptr(dn), n, C.byref(kp),
+                                         dptr(du), dptr(dw)))
+
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        launch()
+    ctx.sync()
+    barrier()
+    torch.cuda.synchronize()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(st):
+                flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            launch()
+            b.record(st)
+            b.synchronize()
+            times.append(a.elapsed_time(b))
+    ctx.sync()
+    torch.cuda.synchronize()
+    barrier()
+    ms = sum(times) / len(times)
+    ms_max = reduce_max(ms, dev)
+    value = world * n * n / (ms_max * 1e-3) / 1e9
+
+    # parity spot check of this run's output against the reference restatement (rows)
+    parity = None
+    if rank == 0 and not args.no_cpu:
+        from oracle.pyoracle import Oracle
+
+        rows = np.r_[0:32, n // 2:n // 2 + 32, n - 32:n]
+        ou, ow = Oracle("or").evaluate_velocities(x[rows], x, f, tq, EPS, MU)
+        gu, gw = du.cpu().numpy()[rows], dw.cpu().numpy()[rows]
+        scale = max(np.abs(ou).max(), np.abs(ow).max())
+        parity = float(max(np.abs(gu - ou).max(), np.abs(gw - ow).max()) / scale)
+
+    # --- e2e through the C-ABI host entry point, pinned host buffers ---
+    hx, hf, hn = (torch.as_tensor(a).pin_memory() for a in (x, f, tq))
+    hu = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+    hw = torch.empty_like(hu)
+    P = C.POINTER(C.c_double)
+
+    def hp(t):
+        return C.cast(t.data_ptr(), P)
+
+    def e2e_call():
+        ctx.check(L.pswim_mrs_velocities_host(ctx.handle, hp(hx), n, hp(hx), hp(hf), hp(hn), n, C.byref(kp),
+                                              hp(hu), hp(hw)))
+
+    for _ in range(max(1, args.warmup)):
+        e2e_call()
+    barrier()
+    e2e_t = []
+    for _ in range(args.steps):
+        with torch.cuda.stream(st):
+            flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_call()
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = reduce_max(sum(e2e_t) / len(e2e_t), dev)
+    e2e_value = world * n * n / e2e_s / 1e9
+    h2d = 4 * n * 3 * 8
+    d2h = 2 * n * 3 * 8
+
+    # --- roofline of the dominant kernel ---
+    achieved = FLOP_PER_PAIR * n * n / (ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "mrs_kernel_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "compute", "pipe": "FP64 FMA (CUDA cores; FP64 is not a dense contraction)",
+                "achieved": achieved, "peak": dfma_peak / 1e12, "unit": "TFLOP/s", "frac": achieved / (dfma_peak / 1e12),
+                "traffic": traffic, "kernel": "mrs_kernel<true>",
+                "flop_per_pair": FLOP_PER_PAIR, "peak_source": "DFMA microbenchmark measured in this run "
+                "(MEASURED_PEAKS.json has no FP64 entry)", "dp_instructions_per_pair": 54.5}
+
+    # --- secondary: simulated RK2 time-steps/s ---
+    time_steps = None
+    if not args.no_steps:
+        time_steps = time_steps_leg(args, world, rank, local, dev)
+
+    # --- HBM-bound rod-side kernels on >= 1e7 elements (rank 0, N=1) ---
+    hbm = None
+    if rank == 0 and world == 1 and not args.no_steps:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from probe_rod import hbm_kernels
+
+        hbm = hbm_kernels(local)
+        for v in hbm.values():
+            v["frac_of_measured_hbm"] = v["GB_per_s"] / _hbm_peak()
+
+    # --- CPU baseline (reference, host cores) ---
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle.pyoracle import LIB_PATHS
+
+        if os.path.exists(LIB_PATHS["ref"]):
+            nt = args.ref_targets
+            ct, cores = cpu_reference_mrs(nt, 3)
+            best = min(ct)
+            cpu = {"value": nt * n / best / 1e9, "unit": "Gpair/s", "cores": cores, "kind": "reference",
+                   "sample": f"best of 3: {nt} targets x {n} sources of the N=16384 workload "
+                             "(oracle/_ref = reference evaluate_velocities, OpenMP)"}
+        else:
+            cpu = {"value": None, "unit": "Gpair/s", "cores": 0, "kind": "reference",
+                   "sample": "oracle/_ref not built on this box"}
+
+    if rank == 0:
+        line = {
+            "metric": "MRS Gpair-interactions/s", "value": value, "unit": "Gpair/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "points": n, "epsilon": EPS, "mu": MU, "targets_equal_sources": True,
+                       "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"replicas{world}"},
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_value, "unit": "Gpair/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": 1e3 * e2e_s, "api": "pswim_mrs_velocities_host (C-ABI)"},
+            "gpu_launches": args.steps,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "parity_rel_err_vs_oracle": parity,
+            "time_steps": time_steps,
+            "hbm_kernels": hbm,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        barrier()
+        dist.destroy_process_group()
+
+
+def time_steps_leg(args, world, rank, local, dev):
+    """Simulated RK2 time-steps/s: serial fine (N=1) or sliced pipelined Parareal (N>1)."""
+    import torch
+
+    from paper_2604_12083_b200 import parareal as pr
+    from paper_2604_12083_b200.device import Context, dptr
+    from paper_2604_12083_b200.scenario import ScenarioConfig, build_initial_state, make_scenario
+
+    sc = make_scenario(ScenarioConfig(rod_count=64, nodes_per_rod=256, epsilon=0.08, fine_dt=1e-6))
+    x0 = build_initial_state(sc)
+    if world == 1:
+        ctx = Context(local, sc)
+        L = ctx.lib
+        dx = torch.as_tensor(x0, device=dev)
+        out = torch.empty_like(dx)
+        steps = args.fine_steps
+        ctx.check(L.pswim_propagate(ctx.handle, dptr(dx), 0.0, 3e-6, 1, 3, 0.0, dptr(out)))  # warm-up
+        st = ctx.torch_stream()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        ctx.check(L.pswim_propagate(ctx.handle, dptr(dx), 0.0, steps * 1e-6, 1, steps, 0.0, dptr(out)))
+        b.record(st)
+        b.synchronize()
+        sec = a.elapsed_time(b) * 1e-3
+        ctx.close()
+        return {"metric": "simulated RK2 time-steps/s", "value": steps / sec, "unit": "steps/s",
+                "config": {"workload": "serial fine RK2, 64 x 256 suspension, eps=0.08, dt=1e-6 (BASELINE configs[2])",
+                           "steps": steps}, "gpu_launches_per_step": 6}
+    # N > 1: one Parareal slice per GPU, NCCL hand-offs
+    fine_steps, coarse_steps = args.fine_steps, max(1, args.fine_steps // 10)
+    plan = pr.ParallelPlan(t0=0.0, horizon=world * fine_steps * 1e-6, intervals=world, workers=world,
+                           max_iterations=args.parareal_iters, tolerance=1e-300, mode=pr.PIPELINED)
+    tr = pr.nccl_transport(local)
+    try:
+        pr.run_sliced_rank(plan, sc, fine_steps, coarse_steps, x0, local, transport=tr)  # warm-up
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = pr.run_sliced_rank(plan, sc, fine_steps, coarse_steps, x0, local, transport=tr)
+        wall = reduce_max(time.perf_counter() - t0, dev)
+    finally:
+        _lib_destroy(tr)
+    return {"metric": "simulated RK2 time-steps/s", "value": world * fine_steps / wall, "unit": "steps/s",
+            "config": {"workload": "pipelined Parareal, one slice per GPU, 64 x 256 suspension (BASELINE configs[3])",
+                       "intervals": world, "fine_rk2_steps_per_interval": fine_steps,
+                       "coarse_euler_steps_per_interval": coarse_steps, "iterations": res.report.iterations_used,
+                       "eta_tilde": res.report.eta_tilde}}
+
+
+def _hbm_peak() -> float:
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback
+
+
+def _lib_destroy(tr):
+    from paper_2604_12083_b200 import _lib
+
+    _lib.lib().pswim_nccl_transport_destroy(tr)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-targets", type=int, default=4096, help="bounded target sample for the CPU legs")
+    ap.add_argument("--fine-steps", type=int, default=50, help="RK2 steps per interval for the time-step leg")
+    ap.add_argument("--parareal-iters", type=int, default=1)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (profiling runs)")
+    ap.add_argument("--no-steps", action="store_true", help="skip the time-step leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

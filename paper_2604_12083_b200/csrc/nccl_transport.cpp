@@ -4,15 +4,62 @@
 // state (12 doubles per node) over NVLink / NVSwitch, and the per-iteration convergence
 // metric is one ncclAllReduce(max) of 2 doubles; every call is stream ordered on the rank
 // driver's communication stream (parareal.cpp).
+//
+// NCCL is resolved at run time (dlopen) instead of at link time: the process may already
+// hold PyTorch's bundled libnccl.so.2 (a newer 2.28) and a link-time dependency on the
+// system 2.27 would otherwise shadow it.  Preference: an already-loaded libnccl.so.2, then
+// the CUDA wheel's copy, then the system library.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
+#include <string>
 
 #include "internal.h"
 
 namespace {
+
+struct NcclApi {
+    bool ok = false;
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+    decltype(&ncclCommDestroy) comm_destroy = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclAllReduce) all_reduce = nullptr;
+};
+
+NcclApi& api() {
+    static NcclApi a;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+        const char* env = std::getenv("PSWIM_NCCL_LIB");
+        if (!h && env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            const char* cands[] = {
+                "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2",
+                "libnccl.so.2",
+                "/usr/lib/x86_64-linux-gnu/libnccl.so.2",
+            };
+            for (const char* c : cands)
+                if ((h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
+        }
+        if (!h) return;
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.send = reinterpret_cast<decltype(a.send)>(dlsym(h, "ncclSend"));
+        a.recv = reinterpret_cast<decltype(a.recv)>(dlsym(h, "ncclRecv"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.send && a.recv && a.all_reduce;
+    });
+    return a;
+}
 
 struct NcclTransport {
     pswim_transport t;  // first member: the C handle points here
@@ -22,22 +69,24 @@ struct NcclTransport {
 
 int nc_send(void* u, const double* buf, int64_t len, int32_t peer, void* st) {
     auto* n = static_cast<NcclTransport*>(u);
-    return ncclSend(buf, static_cast<size_t>(len), ncclDouble, peer, n->comm, static_cast<cudaStream_t>(st)) == ncclSuccess
+    return api().send(buf, static_cast<size_t>(len), ncclDouble, peer, n->comm, static_cast<cudaStream_t>(st)) ==
+                   ncclSuccess
                ? PSWIM_OK
                : PSWIM_ECOMM;
 }
 
 int nc_recv(void* u, double* buf, int64_t len, int32_t peer, void* st) {
     auto* n = static_cast<NcclTransport*>(u);
-    return ncclRecv(buf, static_cast<size_t>(len), ncclDouble, peer, n->comm, static_cast<cudaStream_t>(st)) == ncclSuccess
+    return api().recv(buf, static_cast<size_t>(len), ncclDouble, peer, n->comm, static_cast<cudaStream_t>(st)) ==
+                   ncclSuccess
                ? PSWIM_OK
                : PSWIM_ECOMM;
 }
 
 int nc_allreduce(void* u, double* buf, int64_t len, void* st) {
     auto* n = static_cast<NcclTransport*>(u);
-    return ncclAllReduce(buf, buf, static_cast<size_t>(len), ncclDouble, ncclMax, n->comm,
-                         static_cast<cudaStream_t>(st)) == ncclSuccess
+    return api().all_reduce(buf, buf, static_cast<size_t>(len), ncclDouble, ncclMax, n->comm,
+                            static_cast<cudaStream_t>(st)) == ncclSuccess
                ? PSWIM_OK
                : PSWIM_ECOMM;
 }
@@ -48,14 +97,15 @@ extern "C" {
 
 int pswim_nccl_unique_id(uint8_t* id128) {
     static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+    if (!api().ok || !id128) return PSWIM_ECOMM;
     ncclUniqueId id;
-    if (ncclGetUniqueId(&id) != ncclSuccess) return PSWIM_ECOMM;
+    if (api().get_unique_id(&id) != ncclSuccess) return PSWIM_ECOMM;
     std::memcpy(id128, &id, sizeof id);
     return PSWIM_OK;
 }
 
 pswim_transport* pswim_nccl_transport_create(const uint8_t* id128, int32_t rank, int32_t world, int device) {
-    if (!id128 || rank < 0 || rank >= world) return nullptr;
+    if (!api().ok || !id128 || rank < 0 || rank >= world) return nullptr;
     auto* n = new (std::nothrow) NcclTransport();
     if (!n) return nullptr;
     n->device = device;
@@ -65,7 +115,7 @@ pswim_transport* pswim_nccl_transport_create(const uint8_t* id128, int32_t rank,
     }
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof id);
-    if (ncclCommInitRank(&n->comm, world, id, rank) != ncclSuccess) {
+    if (api().comm_init_rank(&n->comm, world, id, rank) != ncclSuccess) {
         delete n;
         return nullptr;
     }
@@ -81,7 +131,7 @@ pswim_transport* pswim_nccl_transport_create(const uint8_t* id128, int32_t rank,
 void pswim_nccl_transport_destroy(pswim_transport* t) {
     if (!t) return;
     auto* n = static_cast<NcclTransport*>(t->user);
-    if (n->comm) ncclCommDestroy(n->comm);
+    if (n->comm) api().comm_destroy(n->comm);
     delete n;
 }
 
