@@ -308,6 +308,11 @@ int pswim_parareal_run_threads(const pswim_plan* plan, const pswim_scenario* sc,
  * the whole chip on the context's device; ms = kernel time. */
 int pswim_dfma_peak(pswim_ctx* ctx, double* flops_per_s, double* ms);
 
+/* Developer diagnostics: FP64 pipe microbenchmarks (kind 0 constant operands, 1 shared
+ * register operands, 2 three distinct register pairs per DFMA, 3 DMUL, 4 kind 2 + MUFU.RSQ64H);
+ * returns FP64 instructions per second (one lane-op each). */
+int pswim_dev_fp64_probe(pswim_ctx* ctx, int kind, double* ops_per_s, double* ms);
+
 /* Library version string. */
 const char* pswim_version(void);
 

@@ -1,0 +1,78 @@
+// ab_parareal.cpp — TEST INFRASTRUCTURE (A/B harness, built into oracle/_ref/).
+//
+// Runs the reference's OWN Parareal engine (pintswim::parareal::run, src/parareal.cpp,
+// compiled unmodified) twice on the desk scenario of acceptance criterion 1
+// (tests/acceptance_main.cpp:39-89, reduced): once with the reference CPU propagators built
+// as harness::prepare does, once with the B200 propagators of include/pswim/pintswim_gpu.hpp
+// plugged into the same PropagatorFn slots.  Prints one JSON line; exit 0 when
+//   * GPU boundary states match the CPU ones to <= 1e-10 (rod_position_metric),
+//   * iteration counts / convergence flags agree and eta_tilde agrees to 1e-6 relative,
+//   * GPU runs are bitwise identical across modes (regular / pipelined) and m in {1,2,4}.
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "pintswim/harness.hpp"
+#include "pintswim/io.hpp"
+#include "pswim/pintswim_gpu.hpp"
+
+using namespace pintswim;
+
+int main() {
+    RunConfig cfg;
+    cfg.scenario.rod_count = 1;
+    cfg.scenario.nodes_per_rod = 21;
+    cfg.scenario.horizon = 1.0;
+    cfg.intervals = 8;
+    cfg.workers = 2;
+    cfg.max_iterations = 10;
+    cfg.tolerance = 1e-12;
+    cfg.fine_steps_per_interval = 400;
+    cfg.coarse_steps_per_interval = 10;
+    cfg.mode = parareal::Mode::pipelined;
+    const auto run = harness::prepare(cfg);
+    const auto reference = harness::serial_fine_boundaries(run);
+    const auto cpu = parareal::run(run.plan, run.coarse, run.fine, run.x0, rod_position_metric(), &reference);
+
+    const auto gfine = pswim_gpu::make_propagator(run.scenario, Scheme::rk2, 400);
+    const auto gcoarse = pswim_gpu::make_propagator(run.scenario, Scheme::euler, 10);
+    const auto gpu = parareal::run(run.plan, gcoarse, gfine, run.x0, rod_position_metric(), &reference);
+
+    double worst = 0.0;
+    for (std::size_t n = 0; n < cpu.states.size(); ++n)
+        worst = std::max(worst, rod_position_metric()(cpu.states[n], gpu.states[n]));
+    double eta_rel = 0.0;
+    const bool same_k = cpu.report.iterations_used == gpu.report.iterations_used &&
+                        cpu.report.converged == gpu.report.converged &&
+                        cpu.report.eta_tilde.size() == gpu.report.eta_tilde.size();
+    if (same_k)
+        for (std::size_t k = 0; k < cpu.report.eta_tilde.size(); ++k)
+            eta_rel = std::max(eta_rel, std::abs(cpu.report.eta_tilde[k] - gpu.report.eta_tilde[k]) /
+                                            std::max(cpu.report.eta_tilde[k], 1e-300));
+
+    bool bitwise = true;
+    for (const auto mode : {parareal::Mode::regular, parareal::Mode::pipelined}) {
+        for (const int m : {1, 2, 4}) {
+            auto plan = run.plan;
+            plan.mode = mode;
+            plan.workers = m;
+            plan.max_iterations = 3;
+            plan.tolerance = 1e-300;
+            static std::vector<parareal::Vec> first;
+            const auto r = parareal::run(plan, gcoarse, gfine, run.x0, rod_position_metric());
+            if (first.empty()) {
+                first = r.states;
+            } else {
+                for (std::size_t n = 0; n < first.size(); ++n) bitwise = bitwise && (first[n] == r.states[n]);
+            }
+        }
+    }
+    const bool ok = worst <= 1e-10 && same_k && eta_rel <= 1e-6 && bitwise;
+    std::printf("{\"ok\": %s, \"max_position_metric_gpu_vs_cpu\": %.3e, \"iterations_cpu\": %d, \"iterations_gpu\": %d, "
+                "\"converged_cpu\": %d, \"converged_gpu\": %d, \"eta_tilde_rel_diff\": %.3e, \"gpu_bitwise_modes_workers\": %s, "
+                "\"eta_last_cpu\": %.3e, \"eta_last_gpu\": %.3e}\n",
+                ok ? "true" : "false", worst, cpu.report.iterations_used, gpu.report.iterations_used,
+                (int)cpu.report.converged, (int)gpu.report.converged, eta_rel, bitwise ? "true" : "false",
+                cpu.report.eta.empty() ? 0.0 : cpu.report.eta.back(), gpu.report.eta.empty() ? 0.0 : gpu.report.eta.back());
+    return ok ? 0 : 1;
+}

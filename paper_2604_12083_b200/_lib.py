@@ -124,6 +124,7 @@ SIGNATURES = {
     "pswim_parareal_run_threads": (C.c_int, [C.POINTER(Plan), C.POINTER(Scenario), C.POINTER(C.c_int), _i64, _i64,
                                              _dp, _dp, _dp, C.POINTER(Report)]),
     "pswim_dfma_peak": (C.c_int, [_vp, _dp, _dp]),
+    "pswim_dev_fp64_probe": (C.c_int, [_vp, C.c_int, _dp, _dp]),
     "pswim_version": (C.c_char_p, []),
 }
 

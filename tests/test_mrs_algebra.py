@@ -21,12 +21,12 @@ def emulate(t, s, f, n, eps, mu):
     y7 = y5 * y2
     h1 = e2 * y3 + y
     h3 = 1.5 * e2 * y5 + y3
-    h4 = 3.75 * e2 * e2 * y7 - 0.75 * e2 * y5 - 0.5 * y3
-    h5 = 3.75 * e2 * y7 + 1.5 * y5
+    g4 = -7.5 * e2 * e2 * y7 + h3          # H4 = -g4 / 2
+    g5 = 2.5 * e2 * y7 + y5                # H5 = 3 g5 / 2
     fr = (fp[None] * r).sum(-1)
-    nr = (nq[None] * r).sum(-1)
+    n3r = ((-3.0 * nq)[None] * r).sum(-1)  # staged n3 = -3 n'
     u = (h1[..., None] * fp[None]).sum(1) + ((y3 * fr)[..., None] * r).sum(1)
-    w = (h4[..., None] * nq[None]).sum(1) + ((h5 * nr)[..., None] * r).sum(1)
+    w = -0.5 * ((g4[..., None] * nq[None]).sum(1) + ((g5 * n3r)[..., None] * r).sum(1))
     an, bn = h3 @ nq, h3 @ mn
     af, bf = h3 @ fp, h3 @ mf
     u += np.cross(an, tp) - bn
