@@ -285,7 +285,10 @@ def run_ours(args) -> None:
     # --- secondary: simulated RK2 time-steps/s ---
     time_steps = None
     if not args.no_steps:
-        time_steps = time_steps_leg(args, world, rank, local, dev)
+        try:
+            time_steps = time_steps_leg(args, world, rank, local, dev)
+        except Exception as e:  # the MRS line must still be reported
+            time_steps = {"error": f"{type(e).__name__}: {e}"}
 
     # --- HBM-bound rod-side kernels on >= 1e7 elements (rank 0, N=1) ---
     hbm = None

@@ -172,6 +172,12 @@ int pswim_step(pswim_ctx* ctx, int scheme, const double* d_state, double t, doub
 int pswim_propagate(pswim_ctx* ctx, const double* d_in, double t0, double t1, int scheme,
                     int64_t steps_per_interval, double dt, double* d_out);
 
+/* Small systems (N <= 256 nodes) propagate a whole interval in one fused cluster kernel
+ * (state resident in shared memory, MRS partials exchanged through distributed shared
+ * memory), bitwise identical to the per-step launched path.  Enabled by default; returns
+ * the cluster size used for the context's scenario (0 = not eligible). */
+int pswim_set_fused(pswim_ctx* ctx, int enable);
+
 /* Host-buffer propagate (e2e boundary: H2D, propagate, D2H). */
 int pswim_propagate_host(pswim_ctx* ctx, const double* h_in, double t0, double t1, int scheme,
                          int64_t steps_per_interval, double dt, double* h_out);

@@ -195,6 +195,12 @@ int pswim_ctx::propagate_async(const double* d_in, double t0, double t1, int sch
     double dt = 0.0;
     int rc = resolve_steps(t0, t1, spi, dtc, &steps, &dt);
     if (rc) return rc;
+    if (fused_on && !timing_on && fused_cluster_size(rp) > 0) {
+        // the whole interval in one launch, bitwise identical to the loop below
+        const cudaError_t e = fused_propagate_launch(rp, d_out, steps, t0, dt, scheme, d_flags, stream);
+        if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("fused_propagate: ") + cudaGetErrorString(e));
+        return PSWIM_OK;
+    }
     double t = t0;
     for (int64_t i = 0; i < steps; ++i) {
         rc = step(scheme, d_out, t, dt, d_out);
@@ -426,6 +432,12 @@ int pswim_propagate_host(pswim_ctx* ctx, const double* h_in, double t0, double t
     if (rc) return rc;
     CK(cudaMemcpyAsync(h_out, ctx->h_in, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     return ctx->sync();
+}
+
+int pswim_set_fused(pswim_ctx* ctx, int enable) {
+    if (!ctx) return PSWIM_EINVAL;
+    ctx->fused_on = enable != 0;
+    return ctx->has_scenario ? fused_cluster_size(ctx->rp) : 0;
 }
 
 void pswim_timing_enable(pswim_ctx* ctx, int on) {

@@ -39,6 +39,7 @@ struct pswim_ctx {
         int stage;
     };
     bool timing_on = false;
+    bool fused_on = true;  // whole-interval fused kernel for N <= 256 (fused.cu)
     std::vector<TimedStage> open_stages, done_stages;
     double stage_seconds[3] = {0, 0, 0};
 

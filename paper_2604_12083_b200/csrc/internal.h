@@ -61,6 +61,12 @@ cudaError_t correct_launch(const double* xp, const double* gn, const double* go,
                            cudaStream_t st);
 cudaError_t dfma_launch(double* sink, int blocks, int iters, cudaStream_t st);
 
+// ---- fused small-system propagator (fused.cu) ---------------------------------------------
+// Cluster size the fused path uses for this scenario (0 = not eligible: N > 256 or smem).
+int fused_cluster_size(const RodParams& p);
+cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t steps, double t0, double dt, int scheme,
+                                   unsigned* flags, cudaStream_t st);
+
 // ---- host scenario (scenario.cpp) -------------------------------------------------------
 int resolve_scenario(const pswim_scenario* sc, pswim_resolved* out, std::string* err);
 RodParams rod_params(const pswim_scenario* sc, const pswim_resolved& rs);

@@ -129,3 +129,54 @@ def test_quiet_rod_zero_rhs(gpu):
     sc = make_scenario(ScenarioConfig(rod_count=1, nodes_per_rod=21, waveform=WaveformParams(0.0, 2 * np.pi, 1.0)))
     v = rhs(build_initial_state(sc), 0.0, sc)
     assert np.abs(v.u).max() < 1e-13 and np.abs(v.omega).max() < 1e-13
+
+
+@pytest.mark.parametrize("kw,scheme,steps", [(dict(rod_count=1, nodes_per_rod=100), 1, 50),
+                                             (dict(rod_count=1, nodes_per_rod=100), 0, 50),
+                                             (dict(rod_count=1, nodes_per_rod=21), 1, 40),
+                                             (dict(rod_count=4, nodes_per_rod=21, placement=1, lj_well_depth=0.01,
+                                                   seed=2), 1, 20),
+                                             (dict(rod_count=2, nodes_per_rod=128, epsilon=0.08), 1, 10)])
+def test_fused_propagate_bitwise_equals_launched_path(gpu, oracle, kw, scheme, steps):
+    """The fused cluster kernel (N <= 256) reproduces the per-step launched kernels bitwise
+    and the oracle to 1e-10."""
+    from paper_2604_12083_b200.device import Context
+    from paper_2604_12083_b200.propagators import StepperConfig, propagate
+    from paper_2604_12083_b200.scenario import build_initial_state
+    from oracle.pyoracle import Scenario as OS
+
+    sc = scen(**kw)
+    x = build_initial_state(sc)
+    fused = Context(0, sc)
+    plain = Context(0, sc)
+    cs = fused.lib.pswim_set_fused(fused.handle, 1)
+    assert cs >= 1
+    plain.lib.pswim_set_fused(plain.handle, 0)
+    cfg = StepperConfig(0.0, scheme, steps)
+    t1 = steps * 1e-5
+    a = propagate(x, 0.0, t1, cfg, sc, ctx=fused)
+    b = propagate(x, 0.0, t1, cfg, sc, ctx=plain)
+    assert np.array_equal(a, b)
+    want = oracle.propagate(OS.make(**kw), x, 0.0, t1, scheme, steps=steps)
+    assert oracle.position_metric(want, a) < 1e-10
+    fused.close()
+    plain.close()
+
+
+def test_fused_stiffness_and_step_chain(gpu):
+    """Stiffness guard raised from inside the fused kernel; fused propagate equals the chain
+    of single steps (reference test_propagators.cpp:179-191)."""
+    from paper_2604_12083_b200.propagators import StepperConfig, StiffnessError, propagate, step_rk2
+    from paper_2604_12083_b200.scenario import build_initial_state
+
+    sc = scen(rod_count=1, nodes_per_rod=21)
+    x = build_initial_state(sc)
+    horizon = 0.0625
+    manual = x
+    t = 0.0
+    for _ in range(8):
+        manual = step_rk2(manual, t, horizon / 8, sc)
+        t += horizon / 8
+    assert np.array_equal(propagate(x, 0.0, horizon, StepperConfig(0.0, 1, 8), sc), manual)
+    with pytest.raises(StiffnessError):
+        propagate(x, 0.0, 50.0, StepperConfig(0.0, 1, 5), sc)
