@@ -66,10 +66,12 @@ int pswim_ctx::check_flags_after_sync() {
     if (!f) return PSWIM_OK;
     *h_flags = 0;
     cudaMemsetAsync(d_flags, 0, sizeof(unsigned), stream);
-    if (f & kFlagNonFinite) return fail(PSWIM_ENONFINITE, "stokes: non-finite load entry");
-    if (f & kFlagDegenerate) return fail(PSWIM_EDEGENERATE, "internal_loads: degenerate segment (coincident nodes)");
+    // Priority follows the order the reference would throw in: a stiff step aborts before
+    // the next rhs can see its (possibly degenerate / non-finite) result.
     if (f & kFlagStiff)
         return fail(PSWIM_ESTIFF, "time step moved a node more than 10 segment lengths; reduce dt or r");
+    if (f & kFlagDegenerate) return fail(PSWIM_EDEGENERATE, "internal_loads: degenerate segment (coincident nodes)");
+    if (f & kFlagNonFinite) return fail(PSWIM_ENONFINITE, "stokes: non-finite load entry");
     if (f & kFlagAxis) return fail(PSWIM_EINVAL, "from_axis_angle: axis is not a unit vector");
     return fail(PSWIM_ESTATE, "unknown device flag");
 }
