@@ -9,9 +9,11 @@
 //                     (src/rod.cpp:176-195), one thread per node.
 //   sqrt_batched      sqrt_rotation over a batch (rotation.cpp:91-107), smem-staged.
 //   metric / correct  rod_position_metric (io.cpp:49-68), corrected (parareal.cpp:47-54).
+#include <algorithm>
 #include <cmath>
 
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace pswim {
 namespace {
@@ -102,33 +104,231 @@ advance_kernel(const double* __restrict__ state, const double* __restrict__ u, c
 }
 
 // ---------------------------------------------------------------------------------------
-// batched sqrt_rotation: 256 matrices per CTA staged through smem with 16-byte vector
-// loads/stores (AoS 72 B records are not 16-B aligned per thread).
+// advance_state, persistent TMA-bulk pipeline: 256-node chunks of (state, u, w) stream in
+// with cp.async.bulk (2-stage ring, 36 KiB per stage), each thread advances its node in
+// place in shared memory, the new states leave with one bulk store per chunk.
+// ---------------------------------------------------------------------------------------
+constexpr int kAdvBlock = 256;
+constexpr int kAdvStages = 2;
+constexpr uint32_t kAdvStateBytes = kAdvBlock * 12 * sizeof(double);
+constexpr uint32_t kAdvVelBytes = kAdvBlock * 3 * sizeof(double);
+constexpr uint32_t kAdvStageBytes = kAdvStateBytes + 2 * kAdvVelBytes;
+
+__global__ void __launch_bounds__(kAdvBlock, 3)
+advance_tma_kernel(const double* __restrict__ state, const double* __restrict__ u, const double* __restrict__ w,
+                   double dt, double max_disp, int64_t total, double* __restrict__ out,
+                   unsigned* __restrict__ flags) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kAdvStages * kAdvStageBytes);
+    const int64_t nchunks = (total + kAdvBlock - 1) / kAdvBlock;
+    const int64_t nfull = total / kAdvBlock;
+    auto st_of = [&](int s) { return reinterpret_cast<double*>(smem + s * kAdvStageBytes); };
+    auto issue = [&](int s, int64_t c) {
+        double* b = st_of(s);
+        mbar_expect_tx(&full[s], kAdvStageBytes);
+        bulk_load(b, state + 12 * kAdvBlock * c, kAdvStateBytes, &full[s]);
+        bulk_load(b + 12 * kAdvBlock, u + 3 * kAdvBlock * c, kAdvVelBytes, &full[s]);
+        bulk_load(b + 15 * kAdvBlock, w + 3 * kAdvBlock * c, kAdvVelBytes, &full[s]);
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kAdvStages; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int s = 0; s < kAdvStages; ++s) {
+            const int64_t c = blockIdx.x + (int64_t)s * gridDim.x;
+            if (c < nfull) issue(s, c);
+        }
+    unsigned fl = 0;
+    for (int64_t k = 0;; ++k) {
+        const int64_t c = blockIdx.x + k * gridDim.x;
+        if (c >= nchunks) break;
+        const int s = (int)(k % kAdvStages);
+        double* b = st_of(s);
+        if (c < nfull) {
+            mbar_wait(&full[s], (uint32_t)((k / kAdvStages) & 1));
+            const int i = threadIdx.x;
+            fl |= advance_node(b + 12 * i, b + 12 * kAdvBlock + 3 * i, b + 15 * kAdvBlock + 3 * i, dt, max_disp,
+                               b + 12 * i);
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                bulk_store(out + 12 * kAdvBlock * c, b, kAdvStateBytes);
+                bulk_commit();
+                const int64_t cn = blockIdx.x + (k + kAdvStages) * gridDim.x;
+                if (cn < nfull) {
+                    bulk_wait_read<0>();
+                    issue(s, cn);
+                }
+            }
+        } else {
+            const int64_t i = c * kAdvBlock + threadIdx.x;
+            if (i < total) fl |= advance_node(state + 12 * i, u + 3 * i, w + 3 * i, dt, max_disp, out + 12 * i);
+        }
+    }
+    if (fl) atomicOr(flags, fl);
+    if (threadIdx.x == 0) bulk_wait<0>();
+}
+
+// ---------------------------------------------------------------------------------------
+// internal + nodal loads, persistent TMA-bulk pipeline over rods: each rod's packed state
+// (M x 96 B) arrives with one cp.async.bulk into a 2-stage ring while the previous rod is
+// processed; segments then nodes as rod_loads_kernel.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+rod_loads_tma_kernel(RodArgs p, int64_t rods, const double* __restrict__ state, double t, double* __restrict__ pos,
+                     double* __restrict__ fo, double* __restrict__ no, const double* __restrict__ lj,
+                     const double* __restrict__ extra_f, const double* __restrict__ extra_n,
+                     unsigned* __restrict__ flags) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int64_t m = p.m;
+    const uint32_t rod_bytes = (uint32_t)(m * 12 * sizeof(double));
+    double* stage[2] = {reinterpret_cast<double*>(smem), reinterpret_cast<double*>(smem + rod_bytes)};
+    double* seg = reinterpret_cast<double*>(smem + 2 * rod_bytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * rod_bytes + ((6 * (m - 1) * sizeof(double) + 15) & ~15));
+    if (threadIdx.x == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int s = 0; s < 2; ++s) {
+            const int64_t r = blockIdx.x + (int64_t)s * gridDim.x;
+            if (r < rods) {
+                mbar_expect_tx(&full[s], rod_bytes);
+                bulk_load(stage[s], state + 12 * m * r, rod_bytes, &full[s]);
+            }
+        }
+    unsigned fl = 0;
+    for (int64_t k = 0;; ++k) {
+        const int64_t rod = blockIdx.x + k * gridDim.x;
+        if (rod >= rods) break;
+        const int s = (int)(k & 1);
+        const double* xs = stage[s];
+        mbar_wait(&full[s], (uint32_t)((k >> 1) & 1));
+        for (int64_t kk = threadIdx.x; kk + 1 < m; kk += blockDim.x)
+            if (!rod_segment(p, xs, kk, t, seg + 6 * kk)) fl |= kFlagDegenerate;
+        __syncthreads();
+        for (int64_t kk = threadIdx.x; kk < m; kk += blockDim.x) {
+            d3 f, tq;
+            rod_node(p, xs, seg, kk, f, tq);
+            const int64_t g = m * rod + kk;
+            if (lj) f = f + ld3(lj + 3 * g) * p.inv_ds;
+            if (extra_f) {
+                f = f + ld3(extra_f + 3 * g);
+                tq = tq + ld3(extra_n + 3 * g);
+            }
+            st3(pos + 3 * g, ld3(xs + 12 * kk));
+            st3(fo + 3 * g, f);
+            st3(no + 3 * g, tq);
+        }
+        __syncthreads();  // stage s and seg are free again
+        if (threadIdx.x == 0) {
+            const int64_t rn = blockIdx.x + (k + 2) * gridDim.x;
+            if (rn < rods) {
+                mbar_expect_tx(&full[s], rod_bytes);
+                bulk_load(stage[s], state + 12 * m * rn, rod_bytes, &full[s]);
+            }
+        }
+    }
+    if (fl) atomicOr(flags, fl);
+}
+
+// ---------------------------------------------------------------------------------------
+// batched sqrt_rotation, persistent TMA-bulk pipeline: chunks of 256 row-major matrices
+// (18 KiB) stream global -> shared with cp.async.bulk into a 3-stage ring (mbarrier
+// completion), one thread per matrix computes in registers and writes the square root back
+// into the same stage, which leaves with one cp.async.bulk shared -> global store.  A ragged
+// tail chunk (count % 256) and unaligned pointers take the plain-load path.
 // ---------------------------------------------------------------------------------------
 constexpr int kSqrtBlock = 256;
-__global__ void __launch_bounds__(kSqrtBlock)
-sqrt_batched_kernel(const double* __restrict__ r9, int64_t count, double* __restrict__ s9) {
-    __shared__ double2 buf[kSqrtBlock * 9 / 2];
-    double* b = reinterpret_cast<double*>(buf);
-    const int64_t base = (int64_t)blockIdx.x * kSqrtBlock;
-    const int64_t nmat = (count - base) < kSqrtBlock ? (count - base) : kSqrtBlock;
-    const int64_t nd = nmat * 9;
-    const double2* in2 = reinterpret_cast<const double2*>(r9 + base * 9);  // base*9*8 is 16-B aligned (base even)
-    for (int64_t k = threadIdx.x; k < nd / 2; k += kSqrtBlock) buf[k] = __ldcs(in2 + k);
-    if ((nd & 1) && threadIdx.x == 0) b[nd - 1] = r9[base * 9 + nd - 1];
-    __syncthreads();
-    if (threadIdx.x < nmat) {
-        m33 r;
+constexpr int kSqrtStages = 3;
+constexpr uint32_t kSqrtChunkBytes = kSqrtBlock * 9 * sizeof(double);
+
+__device__ __forceinline__ void sqrt_chunk_compute(double* b, int nmat) {
+    m33 r;
+    const bool active = threadIdx.x < nmat;
+    if (active) {
 #pragma unroll
         for (int e = 0; e < 9; ++e) r.m[e] = b[9 * threadIdx.x + e];
+    }
+    __syncthreads();
+    if (active) {
         const m33 s = sqrt_rotation(r);
 #pragma unroll
         for (int e = 0; e < 9; ++e) b[9 * threadIdx.x + e] = s.m[e];
     }
+}
+
+__global__ void __launch_bounds__(kSqrtBlock, 3)
+sqrt_tma_kernel(const double* __restrict__ r9, int64_t count, double* __restrict__ s9) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* stage[kSqrtStages];
+#pragma unroll
+    for (int s = 0; s < kSqrtStages; ++s) stage[s] = reinterpret_cast<double*>(smem + s * kSqrtChunkBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSqrtStages * kSqrtChunkBytes);
+    const int64_t nchunks = (count + kSqrtBlock - 1) / kSqrtBlock;
+    const int64_t nfull = count / kSqrtBlock;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kSqrtStages; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
     __syncthreads();
-    double2* out2 = reinterpret_cast<double2*>(s9 + base * 9);
-    for (int64_t k = threadIdx.x; k < nd / 2; k += kSqrtBlock) __stcs(out2 + k, buf[k]);
-    if ((nd & 1) && threadIdx.x == 0) s9[base * 9 + nd - 1] = b[nd - 1];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kSqrtStages; ++s) {
+            const int64_t c = blockIdx.x + (int64_t)s * gridDim.x;
+            if (c < nfull) {
+                mbar_expect_tx(&full[s], kSqrtChunkBytes);
+                bulk_load(stage[s], r9 + 9 * kSqrtBlock * c, kSqrtChunkBytes, &full[s]);
+            }
+        }
+    }
+    for (int64_t k = 0;; ++k) {
+        const int64_t c = blockIdx.x + k * gridDim.x;
+        if (c >= nchunks) break;
+        const int s = (int)(k % kSqrtStages);
+        double* b = stage[s];
+        if (c < nfull) {
+            mbar_wait(&full[s], (uint32_t)((k / kSqrtStages) & 1));
+            sqrt_chunk_compute(b, kSqrtBlock);
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                bulk_store(s9 + 9 * kSqrtBlock * c, b, kSqrtChunkBytes);
+                bulk_commit();
+                const int64_t cn = blockIdx.x + (k + kSqrtStages) * gridDim.x;
+                if (cn < nfull) {
+                    bulk_wait_read<0>();  // the stage's outgoing store has left shared memory
+                    mbar_expect_tx(&full[s], kSqrtChunkBytes);
+                    bulk_load(b, r9 + 9 * kSqrtBlock * cn, kSqrtChunkBytes, &full[s]);
+                }
+            }
+        } else {
+            const int nmat = (int)(count - c * kSqrtBlock);
+            __syncthreads();
+            for (int e = threadIdx.x; e < 9 * nmat; e += kSqrtBlock) b[e] = r9[9 * kSqrtBlock * c + e];
+            __syncthreads();
+            sqrt_chunk_compute(b, nmat);
+            __syncthreads();
+            for (int e = threadIdx.x; e < 9 * nmat; e += kSqrtBlock) s9[9 * kSqrtBlock * c + e] = b[e];
+        }
+    }
+    if (threadIdx.x == 0) bulk_wait<0>();
+}
+
+// Fallback for pointers that are not 16-byte aligned.
+__global__ void __launch_bounds__(kSqrtBlock)
+sqrt_plain_kernel(const double* __restrict__ r9, int64_t count, double* __restrict__ s9) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    m33 r;
+#pragma unroll
+    for (int e = 0; e < 9; ++e) r.m[e] = r9[9 * i + e];
+    const m33 s = sqrt_rotation(r);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) s9[9 * i + e] = s.m[e];
 }
 
 // ---------------------------------------------------------------------------------------
@@ -187,6 +387,14 @@ __global__ void __launch_bounds__(256) dfma_kernel(double* sink, int iters) {
 
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
 
+// SM count of the current device (persistent grids; results never depend on it).
+inline int num_sms() {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+}
+
 }  // namespace
 
 cudaError_t rod_loads_launch(const RodParams& p, const double* state, double t, double* pos, double* f, double* n,
@@ -198,6 +406,21 @@ cudaError_t rod_loads_launch(const RodParams& p, const double* state, double t, 
     if (!configured) {
         cudaFuncSetAttribute(rod_loads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         configured = true;
+    }
+    const size_t tma_smem = 2 * 96 * (size_t)p.m + ((48 * (size_t)(p.m - 1) + 15) & ~(size_t)15) + 16;
+    const bool aligned = (reinterpret_cast<uintptr_t>(state) & 15) == 0;
+    if (seg_f == nullptr && aligned && p.rods >= 2 * 148 && tma_smem <= 200 * 1024) {
+        static bool tma_configured = false;
+        if (!tma_configured) {
+            cudaFuncSetAttribute(rod_loads_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            tma_configured = true;
+        }
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rod_loads_tma_kernel, 256, tma_smem);
+        const int64_t grid = std::min<int64_t>(p.rods, (int64_t)num_sms() * std::max(per_sm, 1));
+        rod_loads_tma_kernel<<<(unsigned)grid, 256, tma_smem, st>>>(a, p.rods, state, t, pos, f, n, lj, extra_f,
+                                                                   extra_n, flags);
+        return cudaGetLastError();
     }
     rod_loads_kernel<<<(unsigned)p.rods, 256, smem, st>>>(a, state, t, pos, f, n, seg_f, seg_n, lj, extra_f, extra_n,
                                                          flags);
@@ -213,13 +436,44 @@ cudaError_t lj_launch(const RodParams& p, const double* state, double* forces, c
 cudaError_t advance_launch(const RodParams& p, const double* state, const double* u, const double* w, double dt,
                            double* out, unsigned* flags, cudaStream_t st) {
     const int64_t total = p.rods * p.m;
-    advance_kernel<<<grid_for(total, 256), 256, 0, st>>>(state, u, w, dt, 10.0 * p.ds, total, out, flags);
+    const bool aligned = ((reinterpret_cast<uintptr_t>(state) | reinterpret_cast<uintptr_t>(u) |
+                           reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    if (!aligned || total < 4 * kAdvBlock) {
+        advance_kernel<<<grid_for(total, 256), 256, 0, st>>>(state, u, w, dt, 10.0 * p.ds, total, out, flags);
+        return cudaGetLastError();
+    }
+    const size_t smem = kAdvStages * kAdvStageBytes + kAdvStages * sizeof(uint64_t);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(advance_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    const int64_t nchunks = (total + kAdvBlock - 1) / kAdvBlock;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, advance_tma_kernel, kAdvBlock, smem);
+    const int64_t grid = std::min<int64_t>(nchunks, (int64_t)num_sms() * std::max(per_sm, 1));
+    advance_tma_kernel<<<(unsigned)grid, kAdvBlock, smem, st>>>(state, u, w, dt, 10.0 * p.ds, total, out, flags);
     return cudaGetLastError();
 }
 
 cudaError_t sqrt_batched_launch(const double* r9, int64_t count, double* s9, cudaStream_t st) {
     if (count == 0) return cudaSuccess;
-    sqrt_batched_kernel<<<grid_for(count, kSqrtBlock), kSqrtBlock, 0, st>>>(r9, count, s9);
+    const bool aligned = ((reinterpret_cast<uintptr_t>(r9) | reinterpret_cast<uintptr_t>(s9)) & 15) == 0;
+    if (!aligned) {
+        sqrt_plain_kernel<<<grid_for(count, kSqrtBlock), kSqrtBlock, 0, st>>>(r9, count, s9);
+        return cudaGetLastError();
+    }
+    const size_t smem = kSqrtStages * kSqrtChunkBytes + kSqrtStages * sizeof(uint64_t);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(sqrt_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    const int64_t nchunks = (count + kSqrtBlock - 1) / kSqrtBlock;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sqrt_tma_kernel, kSqrtBlock, smem);
+    const int64_t grid = std::min<int64_t>(nchunks, (int64_t)num_sms() * std::max(per_sm, 1));  // persistent
+    sqrt_tma_kernel<<<(unsigned)grid, kSqrtBlock, smem, st>>>(r9, count, s9);
     return cudaGetLastError();
 }
 
