@@ -366,9 +366,11 @@ def time_steps_leg(args, world, rank, local, dev):
         b.synchronize()
         sec = a.elapsed_time(b) * 1e-3
         ctx.close()
-        return {"metric": "simulated RK2 time-steps/s", "value": steps / sec, "unit": "steps/s",
-                "config": {"workload": "serial fine RK2, 64 x 256 suspension, eps=0.08, dt=1e-6 (BASELINE configs[2])",
-                           "steps": steps}, "gpu_launches_per_step": 6}
+        leg = {"metric": "simulated RK2 time-steps/s", "value": steps / sec, "unit": "steps/s",
+               "config": {"workload": "serial fine RK2, 64 x 256 suspension, eps=0.08, dt=1e-6 (BASELINE configs[2])",
+                          "steps": steps}, "gpu_launches_per_step": 6}
+        leg["flagellum"] = flagellum_leg(args, local, dev)
+        return leg
     # N > 1: one Parareal slice per GPU, NCCL hand-offs
     fine_steps, coarse_steps = args.fine_steps, max(1, args.fine_steps // 10)
     plan = pr.ParallelPlan(t0=0.0, horizon=world * fine_steps * 1e-6, intervals=world, workers=world,
@@ -388,6 +390,51 @@ def time_steps_leg(args, world, rank, local, dev):
                        "intervals": world, "fine_rk2_steps_per_interval": fine_steps,
                        "coarse_euler_steps_per_interval": coarse_steps, "iterations": res.report.iterations_used,
                        "eta_tilde": res.report.eta_tilde}}
+
+
+def flagellum_leg(args, local, dev):
+    """BASELINE configs[0]: one 100-node flagellum, serial fine RK2 (dt = 1e-6): fused
+    single-cluster propagate kernel vs the reference's own propagate on the host cores."""
+    import torch
+
+    from paper_2604_12083_b200.device import Context, dptr
+    from paper_2604_12083_b200.scenario import ScenarioConfig, build_initial_state, make_scenario
+
+    kw = dict(rod_count=1, nodes_per_rod=100)
+    sc = make_scenario(ScenarioConfig(**kw))
+    x0 = build_initial_state(sc)
+    ctx = Context(local, sc)
+    cs = ctx.lib.pswim_set_fused(ctx.handle, 1)
+    dx = torch.as_tensor(x0, device=dev)
+    out = torch.empty_like(dx)
+    L = ctx.lib
+    ctx.check(L.pswim_propagate(ctx.handle, dptr(dx), 0.0, 1e-5, 1, 10, 0.0, dptr(out)))
+    steps = 20000
+    st = ctx.torch_stream()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    ctx.check(L.pswim_propagate(ctx.handle, dptr(dx), 0.0, steps * 1e-6, 1, steps, 0.0, dptr(out)))
+    b.record(st)
+    b.synchronize()
+    gpu = steps / (a.elapsed_time(b) * 1e-3)
+    ctx.close()
+    leg = {"metric": "simulated RK2 time-steps/s", "value": gpu, "unit": "steps/s",
+           "config": {"workload": "single flagellum, 1 x 100 nodes, serial fine RK2, dt=1e-6 (BASELINE configs[0])",
+                      "steps": steps, "kernel": f"fused propagate, cluster of {cs} CTAs, 1 launch per interval"}}
+    if not args.no_cpu:
+        from oracle.pyoracle import LIB_PATHS, Oracle, Scenario as OS
+
+        if os.path.exists(LIB_PATHS["ref"]):
+            ref = Oracle("ref")
+            osc = OS.make(**kw)
+            csteps = 2000
+            t0 = time.perf_counter()
+            ref.propagate(osc, x0, 0.0, csteps * 1e-6, 1, steps=csteps)
+            cpu = csteps / (time.perf_counter() - t0)
+            leg["cpu_baseline"] = {"value": cpu, "unit": "steps/s", "cores": ref.max_threads_(), "kind": "reference",
+                                   "sample": f"{csteps} RK2 steps of the same flagellum (reference propagate, OpenMP)"}
+    return leg
 
 
 def _hbm_peak() -> float:

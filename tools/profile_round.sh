@@ -9,3 +9,7 @@ ncu --set full --clock-control none --import-source on -k regex:mrs_kernel -s 3 
     python tools/probe_mrs.py 16384 > gpurun_out/ncu_mrs.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"rod_loads|advance|sqrt_batched" -c 6 -o gpurun_out/rod_full -f \
     python tools/probe_rod.py > gpurun_out/ncu_rod.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"rod_loads_tma|advance_tma|sqrt_tma" -c 3 -o gpurun_out/tma_full -f \
+    python tools/probe_rod.py > gpurun_out/ncu_tma.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"fused_kernel" -s 1 -c 1 -o gpurun_out/fused_full -f \
+    python tools/probe_steps.py > gpurun_out/ncu_fused.log 2>&1
