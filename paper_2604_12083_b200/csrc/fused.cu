@@ -6,10 +6,10 @@
 // cluster with the state resident in shared memory:
 //   * every CTA redundantly holds the full state and redundantly does the O(N) phases
 //     (segment loads with sqrt_rotation, nodal loads, LJ, source staging, advance);
-//   * the O(N^2) MRS work items (target i, source chunk c) are split across the CTAs of the
-//     cluster; each item's 6 partial velocities are pushed to every CTA through distributed
-//     shared memory, one cluster barrier per rhs (partials double-buffered), and every CTA
-//     reduces the chunks in fixed order.
+//   * the O(N^2) MRS is split across the CTAs of the cluster by target: each CTA computes
+//     its targets' (target, source chunk) items, reduces the chunk partials in fixed order
+//     in its own shared memory, and pushes each target's 6 velocities to every CTA through
+//     distributed shared memory; one cluster barrier per rhs (velocities double-buffered).
 // All per-element arithmetic is the kernels.cuh routines of the launched path, and the MRS
 // decomposition (origin, chunk boundaries, chunk order) is the one mrs_plan picks for the
 // same N, so a fused propagate is bitwise identical to the multi-kernel one.
@@ -35,7 +35,7 @@ struct FusedArgs {
     double max_disp;
     // shared-memory offsets (doubles)
     int off_x, off_xm, off_pos, off_f, off_n, off_seg, off_lj, off_rec, off_part, off_vel;
-    int part_stride;  // doubles per partial buffer (chunks * n * 6)
+    int part_stride;  // unused (kept for layout clarity)
 };
 
 template <int CS>
@@ -49,8 +49,7 @@ __device__ __forceinline__ void cluster_barrier() {
 
 // rhs (propagators.cpp:38-91) of the state `xs` at time t into vel[6 n] = (u, w) per node.
 template <int CS>
-__device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, double t, double* vel, int parity,
-                          unsigned& fl) {
+__device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, double t, double* vel, unsigned& fl) {
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n, m = a.m, nseg = a.rods * (m - 1);
     double* pos = sm + a.off_pos;
     double* fo = sm + a.off_f;
@@ -58,7 +57,6 @@ __device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, doub
     double* seg = sm + a.off_seg;
     double* ljf = sm + a.off_lj;
     double2* rec = reinterpret_cast<double2*>(sm + a.off_rec);
-    double* part = sm + a.off_part + parity * a.part_stride;
 
     for (int s = tid; s < nseg; s += bs) {
         const int r = s / (m - 1), k = s % (m - 1);
@@ -95,13 +93,15 @@ __device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, doub
         for (int q = 0; q < 9; ++q) rec[q * N + j] = r[q];
     }
     __syncthreads();
-    // MRS items (i, c), split over the cluster
-    const int items = a.chunks * N;
+    // MRS: this CTA owns targets [i0, i1); items (target, source chunk) computed here, the
+    // chunk partials reduced locally in fixed order (mrs.cu's last-CTA reduction), and each
+    // target's 6 velocities pushed to every CTA of the cluster through DSMEM.
     const int rank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
-    const int per = (items + CS - 1) / CS;
-    const int w0 = rank * per, w1 = min(items, w0 + per);
-    for (int w = w0 + tid; w < w1; w += bs) {
-        const int c = w / N, i = w % N;
+    const int tpc = (N + CS - 1) / CS;
+    const int i0 = rank * tpc, i1 = min(N, i0 + tpc), nloc = max(0, i1 - i0);
+    double* lpart = sm + a.off_part;  // [chunks][tpc][6]
+    for (int w = tid; w < nloc * a.chunks; w += bs) {
+        const int c = w / nloc, il = w % nloc, i = i0 + il;
         const int j0 = (int)((int64_t)c * N / a.chunks), j1 = (int)((int64_t)(c + 1) * N / a.chunks);
         const double tx = pos[3 * i] - ox, ty = pos[3 * i + 1] - oy, tz = pos[3 * i + 2] - oz;
         MrsAcc acc;
@@ -113,32 +113,32 @@ __device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, doub
                      a.mc.c25e2);
         double out[6];
         mrs_finish(acc, tx, ty, tz, out);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) lpart[(c * tpc + il) * 6 + q] = out[q];
+    }
+    __syncthreads();
+    for (int il = tid; il < nloc; il += bs) {
+        double sum[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) sum[q] = lpart[il * 6 + q];
+        for (int c = 1; c < a.chunks; ++c)
+#pragma unroll
+            for (int q = 0; q < 6; ++q) sum[q] += lpart[(c * tpc + il) * 6 + q];
+        const int i = i0 + il;
         if constexpr (CS > 1) {
             cg::cluster_group cl = cg::this_cluster();
 #pragma unroll 1
             for (int rr = 0; rr < CS; ++rr) {
-                double* dst = cl.map_shared_rank(part, rr) + (size_t)(c * N + i) * 6;
+                double* dst = cl.map_shared_rank(vel, rr) + 6 * i;
 #pragma unroll
-                for (int q = 0; q < 6; ++q) dst[q] = out[q];
+                for (int q = 0; q < 6; ++q) dst[q] = sum[q];
             }
         } else {
 #pragma unroll
-            for (int q = 0; q < 6; ++q) part[(c * N + i) * 6 + q] = out[q];
+            for (int q = 0; q < 6; ++q) vel[6 * i + q] = sum[q];
         }
     }
     cluster_barrier<CS>();
-    // fixed-order chunk reduction (mrs.cu last-CTA reduction)
-    for (int i = tid; i < N; i += bs) {
-        double s[6];
-#pragma unroll
-        for (int q = 0; q < 6; ++q) s[q] = part[i * 6 + q];
-        for (int c = 1; c < a.chunks; ++c)
-#pragma unroll
-            for (int q = 0; q < 6; ++q) s[q] += part[(c * N + i) * 6 + q];
-#pragma unroll
-        for (int q = 0; q < 6; ++q) vel[6 * i + q] = s[q];
-    }
-    __syncthreads();
 }
 
 template <int CS>
@@ -149,14 +149,16 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n;
     double* x = sm + a.off_x;
     double* xm = sm + a.off_xm;
-    double* vel = sm + a.off_vel;
     for (int k = tid; k < 12 * N; k += bs) x[k] = state[k];
     __syncthreads();
     unsigned fl = 0;
     int parity = 0;
     double t = t0;
+    // velocities are double-buffered: a CTA that runs ahead pushes the next rhs into the
+    // other buffer while slower CTAs still read this one (the next cluster barrier orders it)
     for (int64_t s = 0; s < steps; ++s) {
-        fused_rhs<CS>(a, sm, x, t, vel, parity, fl);
+        double* vel = sm + a.off_vel + parity * 6 * N;
+        fused_rhs<CS>(a, sm, x, t, vel, fl);
         parity ^= 1;
         if (scheme == PSWIM_EULER) {
             for (int i = tid; i < N; i += bs)
@@ -167,7 +169,8 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
             for (int i = tid; i < N; i += bs)
                 fl |= advance_node(x + 12 * i, vel + 6 * i, vel + 6 * i + 3, 0.5 * dt, a.max_disp, xm + 12 * i);
             __syncthreads();
-            fused_rhs<CS>(a, sm, xm, t + 0.5 * dt, vel, parity, fl);
+            vel = sm + a.off_vel + parity * 6 * N;
+            fused_rhs<CS>(a, sm, xm, t + 0.5 * dt, vel, fl);
             parity ^= 1;
             for (int i = tid; i < N; i += bs)
                 fl |= advance_node(x + 12 * i, vel + 6 * i, vel + 6 * i + 3, dt, a.max_disp, x + 12 * i);
@@ -213,12 +216,12 @@ int fused_cluster_size(const RodParams& p) {
     const int64_t n = p.rods * p.m;
     if (n > 256 || n < 2) return 0;
     const MrsPlan plan = mrs_plan(n, n);
-    const int64_t items = plan.chunks * n;
     int cs = 1;
-    while (cs < 8 && items / (2 * cs) >= 48) cs *= 2;
-    // shared memory: x, xm (12n each), pos/f/n/lj (3n each), seg (6 segs), rec (18n),
-    // partials (2 x chunks x n x 6), vel (6n)
-    const int64_t doubles = 24 * n + 12 * n + 6 * p.rods * (p.m - 1) + 18 * n + 2 * plan.chunks * n * 6 + 6 * n + 8;
+    while (cs < 8 && (n + 2 * cs - 1) / (2 * cs) >= 12) cs *= 2;  // >= 12 targets per CTA
+    const int64_t tpc = (n + cs - 1) / cs;
+    // shared memory: x, xm (12n each), pos/f/n/lj (3n each), seg, rec (18n), local partials
+    // (chunks x tpc x 6), velocities (2 x 6n)
+    const int64_t doubles = 24 * n + 12 * n + 6 * p.rods * (p.m - 1) + 18 * n + plan.chunks * tpc * 6 + 12 * n + 16;
     if (doubles * 8 > 220 * 1024) return 0;
     return cs;
 }
@@ -253,9 +256,10 @@ cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t st
     a.off_seg = take(6 * a.rods * (a.m - 1));
     a.off_lj = take(3 * a.n);
     a.off_rec = take(18 * a.n);
-    a.part_stride = (plan.chunks * a.n * 6 + 1) & ~1;
-    a.off_part = take(2 * a.part_stride);
-    a.off_vel = take(6 * a.n);
+    const int tpc = (a.n + cs - 1) / cs;
+    a.part_stride = 0;
+    a.off_part = take(plan.chunks * tpc * 6);
+    a.off_vel = take(12 * a.n);
     const size_t smem = (size_t)off * sizeof(double);
     switch (cs) {
         case 1: return launch_cs<1>(a, smem, state, steps, t0, dt, scheme, flags, st);
