@@ -422,6 +422,7 @@ def flagellum_leg(args, local, dev):
     leg = {"metric": "simulated RK2 time-steps/s", "value": gpu, "unit": "steps/s",
            "config": {"workload": "single flagellum, 1 x 100 nodes, serial fine RK2, dt=1e-6 (BASELINE configs[0])",
                       "steps": steps, "kernel": f"fused propagate, cluster of {cs} CTAs, 1 launch per interval"}}
+    leg["parareal_1gpu"] = parareal_1gpu_leg(sc, x0, local)
     if not args.no_cpu:
         from oracle.pyoracle import LIB_PATHS, Oracle, Scenario as OS
 
@@ -435,6 +436,45 @@ def flagellum_leg(args, local, dev):
             leg["cpu_baseline"] = {"value": cpu, "unit": "steps/s", "cores": ref.max_threads_(), "kind": "reference",
                                    "sample": f"{csteps} RK2 steps of the same flagellum (reference propagate, OpenMP)"}
     return leg
+
+
+def parareal_1gpu_leg(sc, x0, local, n=8, fine=1000, coarse=100):
+    """Time-parallel on ONE B200: a small system leaves most SMs idle, so the n fine solves
+    of a Parareal iteration run concurrently (fused cluster kernels on n+1 engine lanes).
+    Simulated steps/s = n * fine / wall; eta = error vs the serial fine solution."""
+    from paper_2604_12083_b200 import parareal as pr
+
+    T = n * fine * 1e-6
+    plan = pr.ParallelPlan(horizon=T, intervals=n, workers=n + 1, max_iterations=1, tolerance=1e-300,
+                           mode=pr.PIPELINED)
+    serial = pr.run_gpu(pr.ParallelPlan(horizon=T, intervals=n, workers=1, max_iterations=n, tolerance=1e-300),
+                        sc, fine, coarse, x0, device=local)  # k = n: exact serial fine boundaries
+    # serial fine wall time: the same n fine propagations back to back
+    import torch
+
+    from paper_2604_12083_b200.device import Context, dptr
+
+    ctx = Context(local, sc)
+    cur = torch.as_tensor(x0, device=f"cuda:{local}")
+    out = torch.empty_like(cur)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(n):
+        ctx.check(ctx.lib.pswim_propagate(ctx.handle, dptr(cur), plan.boundary_time(i), plan.boundary_time(i + 1), 1,
+                                          fine, 0.0, dptr(out)))
+        cur, out = out, cur
+    serial_wall = time.perf_counter() - t0
+    ctx.close()
+    out = {}
+    for l in (1, 2):
+        plan.max_iterations = l
+        pr.run_gpu(plan, sc, fine, coarse, x0, device=local)  # warm-up
+        res = pr.run_gpu(plan, sc, fine, coarse, x0, reference=serial.states, device=local)
+        out[f"l{l}"] = {"value": n * fine / res.report.wall_seconds, "unit": "steps/s",
+                        "speedup_vs_serial_fine": serial_wall / res.report.wall_seconds, "eta": res.report.eta[-1]}
+    return {"workload": f"pipelined Parareal on one B200, flagellum 1x100, n={n} intervals x {fine} RK2 "
+                        f"(coarse {coarse} Euler), {n + 1} engine lanes", "serial_fine_steps_per_s": n * fine / serial_wall,
+            **out}
 
 
 def _hbm_peak() -> float:

@@ -126,3 +126,76 @@ def test_mrs_empty(gpu):
     assert e.u.shape == (0, 3)
     z = evaluate_velocities(np.ones((4, 3)), np.zeros((0, 3)), LoadSet(np.zeros((0, 3)), np.zeros((0, 3))), KernelParams())
     assert np.all(z.u == 0.0)
+
+
+def test_mrs_linearity_permutation_curl(gpu):
+    """test_stokes.cpp:154-206 and :279-302 on the GPU operator: linearity in the loads,
+    source-permutation invariance (< 1e-12), and omega = curl(u)/2 by central differences
+    (< 1e-4)."""
+    from paper_2604_12083_b200.stokes import KernelParams, LoadSet, evaluate_velocities
+
+    rng = np.random.default_rng(21)
+    nodes = rng.uniform(-1, 1, (10, 3))
+    kp = KernelParams(0.2, 1.0)
+    la = (rng.uniform(-1, 1, (10, 3)), rng.uniform(-1, 1, (10, 3)))
+    lb = (rng.uniform(-1, 1, (10, 3)), rng.uniform(-1, 1, (10, 3)))
+    al, be = 0.7, -1.3
+    combo = LoadSet(al * la[0] + be * lb[0], al * la[1] + be * lb[1])
+    fa = evaluate_velocities(nodes, nodes, LoadSet(*la), kp)
+    fb = evaluate_velocities(nodes, nodes, LoadSet(*lb), kp)
+    fc = evaluate_velocities(nodes, nodes, combo, kp)
+    scale = np.abs(fc.u).max()
+    assert np.abs(fc.u - (al * fa.u + be * fb.u)).max() / scale < 1e-12
+    assert np.abs(fc.omega - (al * fa.omega + be * fb.omega)).max() / scale < 1e-12
+
+    src = rng.uniform(-1, 1, (15, 3))
+    f, n = rng.uniform(-1, 1, (15, 3)), rng.uniform(-1, 1, (15, 3))
+    tg = rng.uniform(-1, 1, (6, 3))
+    kp = KernelParams(0.3, 1.0)
+    base = evaluate_velocities(tg, src, LoadSet(f, n), kp)
+    perm = rng.permutation(15)
+    sh = evaluate_velocities(tg, src[perm], LoadSet(f[perm], n[perm]), kp)
+    scale = np.abs(base.u).max()
+    assert np.abs(base.u - sh.u).max() / scale < 1e-12 and np.abs(base.omega - sh.omega).max() / scale < 1e-12
+
+    src = rng.uniform(-0.5, 0.5, (6, 3))
+    f, n = rng.uniform(-1, 1, (6, 3)), rng.uniform(-1, 1, (6, 3))
+    kp = KernelParams(0.2, 1.4)
+    h = 1e-4 * kp.epsilon
+    for _ in range(10):
+        p = rng.uniform(-0.8, 0.8, 3)
+        pts = np.array([p + h * e for e in np.eye(3)] + [p - h * e for e in np.eye(3)] + [p])
+        v = evaluate_velocities(pts, src, LoadSet(f, n), kp)
+        du = [(v.u[k] - v.u[3 + k]) / (2 * h) for k in range(3)]
+        half_curl = 0.5 * np.array([du[1][2] - du[2][1], du[2][0] - du[0][2], du[0][1] - du[1][0]])
+        w = v.omega[6]
+        assert np.linalg.norm(w - half_curl) / np.linalg.norm(w) < 1e-4
+
+
+def test_mrs_equals_grand_mobility_matvec(gpu, oracle):
+    """test_stokes.cpp:237-276: the dense 6N x 6N mobility (reference assemble_grand_mobility,
+    oracle restatement) applied to the loads equals the GPU operator (< 1e-12)."""
+    from paper_2604_12083_b200.stokes import KernelParams, LoadSet, evaluate_velocities
+
+    rng = np.random.default_rng(55)
+    nodes = rng.uniform(-0.6, 0.6, (12, 3))
+    f, n = rng.uniform(-1, 1, (12, 3)), rng.uniform(-1, 1, (12, 3))
+    m = oracle.grand_mobility(nodes, 0.4, 1.9)
+    x = np.concatenate([f, n], axis=1).reshape(-1)
+    y = (m @ x).reshape(12, 6)
+    got = evaluate_velocities(nodes, nodes, LoadSet(f, n), KernelParams(0.4, 1.9))
+    scale = np.abs(got.u).max()
+    assert np.abs(y[:, :3] - got.u).max() / scale < 1e-12
+    assert np.abs(y[:, 3:] - got.omega).max() / scale < 1e-12
+
+
+def test_mrs_golden_vectors(gpu, golden):
+    """Reference golden outputs (tests/golden/golden.npz, generated from the reference)."""
+    from paper_2604_12083_b200.stokes import KernelParams, LoadSet, evaluate_velocities
+
+    x = golden["mrs1k_x"]
+    got = evaluate_velocities(x, x, LoadSet(golden["mrs1k_f"], golden["mrs1k_n"]), KernelParams(0.1, 1.0))
+    assert rel_err(got, (golden["mrs1k_u"], golden["mrs1k_w"])) < TOL
+    nd = golden["mrs12_nodes"]
+    got = evaluate_velocities(nd, nd, LoadSet(golden["mrs12_f"], golden["mrs12_n"]), KernelParams(0.15, 2.3))
+    assert rel_err(got, (golden["mrs12_dense_u"], golden["mrs12_dense_w"])) < 1e-12

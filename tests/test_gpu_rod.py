@@ -132,3 +132,70 @@ def test_lj_matches_oracle(gpu, oracle):
     want = oracle.lj_repulsion(x, 12, 51, 0.01, sc.lj_sigma, sc.lj_self_exclusion)
     assert np.abs(want).max() > 0
     assert np.max(np.abs(got - want)) <= 1e-12 * np.abs(want).max()
+
+
+def test_rod_energy_gradient_and_objectivity(gpu, oracle):
+    """test_rod.cpp:126-182 / acceptance C8 on the GPU loads: f = -dE/dx by central differences
+    of the reference's discrete elastic energy (< 1e-6), and frame objectivity under a global
+    rotation (< 1e-10)."""
+    from paper_2604_12083_b200.rod import rod_loads
+    from paper_2604_12083_b200.scenario import MaterialParams, ScenarioConfig, WaveformParams, make_scenario
+
+    mat6 = [0.8, 0.8, 1.2, 3.0, 3.0, 5.0]
+    wave3 = [0.2, 1.5, 1.0]
+    sc = make_scenario(ScenarioConfig(rod_count=1, nodes_per_rod=9, material=MaterialParams(*mat6),
+                                      waveform=WaveformParams(*wave3)))
+    rng = np.random.default_rng(2023)
+    ds = 1.0 / 8
+    t = 0.25
+    hstep = 3e-6 * ds
+    for _ in range(5):
+        rod = perturbed_rod(oracle, 9, 1.0, rng, 0.08, 0.25)
+        f, n, _, _ = rod_loads(rod.reshape(-1), t, sc)
+        scale = np.abs(f).max()
+        worst = 0.0
+        for k in range(9):
+            for c in range(3):
+                rp = rod.copy()
+                rp[k, c] += hstep
+                rm = rod.copy()
+                rm[k, c] -= hstep
+                want = -(oracle.elastic_energy(rp, 1.0, mat6, wave3, t) - oracle.elastic_energy(rm, 1.0, mat6, wave3, t)) / (2 * hstep * ds)
+                worst = max(worst, abs(f[k, c] - want))
+        assert worst / scale < 1e-6
+        q = oracle.from_axis_angle(np.array([0.3, -0.4, 0.866]) / np.linalg.norm([0.3, -0.4, 0.866]), 1.234)
+        rot = rod.copy()
+        for blk in range(4):
+            rot[:, 3 * blk:3 * blk + 3] = rod[:, 3 * blk:3 * blk + 3] @ q.T
+        f2, n2, _, _ = rod_loads(rot.reshape(-1), t, sc)
+        assert np.abs(f2 - f @ q.T).max() / scale < 1e-10
+        assert np.abs(n2 - n @ q.T).max() / scale < 1e-10
+
+
+def test_lj_pair_law_and_antisymmetry(gpu):
+    """test_rod.cpp:184-254: LJ force vanishes at the cutoff, magnitude 24 w / sigma at r =
+    sigma (repulsive), isolated pairs bitwise antisymmetric."""
+    from paper_2604_12083_b200.rod import lj_repulsion
+    from paper_2604_12083_b200.scenario import ScenarioConfig, make_scenario
+
+    sigma, well = 0.5, 2.0
+    sc = make_scenario(ScenarioConfig(rod_count=2, nodes_per_rod=3, rod_length=0.1, lj_well_depth=well,
+                                      lj_sigma=sigma))
+
+    def two_rods(d):
+        x = np.zeros((6, 12))
+        x[:, 3:6] = [0, 1, 0]
+        x[:, 6:9] = [0, 0, 1]
+        x[:, 9:12] = [1, 0, 0]
+        for k in range(3):
+            x[k, 0:3] = [k * 100.0, 0, 0]
+            x[3 + k, 0:3] = [k * 100.0, d, 0]
+        return x.reshape(-1)
+
+    rc = 2 ** (1 / 6) * sigma
+    assert np.all(lj_repulsion(two_rods(rc), sc) == 0.0)
+    f = lj_repulsion(two_rods(sigma), sc)
+    assert abs(np.linalg.norm(f[0]) - 24 * well / sigma) < 1e-12 * 24 * well / sigma
+    assert f[0, 1] < 0
+    f = lj_repulsion(two_rods(0.9 * sigma), sc)
+    assert np.array_equal(f[0], -f[3])
