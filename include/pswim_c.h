@@ -274,6 +274,8 @@ typedef struct pswim_transport {
     int (*recv)(void* user, double* buf, int64_t len, int32_t peer, void* stream);
     /* in-place elementwise max over ranks of `len` doubles */
     int (*allreduce_max)(void* user, double* buf, int64_t len, void* stream);
+    /* recv[r * count + i] = send_of_rank_r[i] for every rank r (rank-major) */
+    int (*allgather)(void* user, const double* send, double* recv, int64_t count, void* stream);
 } pswim_transport;
 
 /* Rank driver: rank p owns interval p+1 of a plan with intervals == world.  Runs the
@@ -300,6 +302,22 @@ int pswim_nccl_unique_id(uint8_t* id128);
 pswim_transport* pswim_nccl_transport_create(const uint8_t* id128, int32_t rank, int32_t world,
                                              int device);
 void pswim_nccl_transport_destroy(pswim_transport* tr);
+
+/* In-process transports: `world` ranks as threads of one process (any device mix).  Returns
+ * an array of `world` transports (index = rank); hand-offs are stream-ordered peer copies +
+ * events, collectives host barriers.  `len` / `slots` size the send/recv staging (doubles per
+ * message, messages per link). */
+pswim_transport* pswim_threads_transports_create(int32_t world, const int* devices, int64_t len, int32_t slots);
+void pswim_threads_transports_destroy(pswim_transport* trs);
+
+/* ---- space-parallel MRS ------------------------------------------ */
+/* propagate with the O(N^2) MRS sharded over the transport's ranks: every rank holds the full
+ * state and does the O(N) rod loads / advance redundantly, computes the velocities of its own
+ * 256-target blocks of the single-GPU launch plan, and all-gathers (u, omega) once per rhs
+ * (48 B/node).  Bitwise identical to pswim_propagate on one GPU.  All ranks call it together. */
+int pswim_propagate_sharded(pswim_ctx* ctx, const pswim_transport* tr, const double* d_in, double t0,
+                            double t1, int scheme, int64_t steps_per_interval, double dt,
+                            double* d_out);
 
 /* In-process transport: `world` slice ranks as threads of one process, each on its own
  * context (any device mix), hand-offs by stream-ordered peer copies + events. */

@@ -74,11 +74,12 @@ PROPAGATOR_FN = C.CFUNCTYPE(C.c_int, _vp, C.c_double, C.c_double, _dp, _dp, _i64
 SEND_FN = C.CFUNCTYPE(C.c_int, _vp, _dp, _i64, _i32, _vp)
 RECV_FN = C.CFUNCTYPE(C.c_int, _vp, _dp, _i64, _i32, _vp)
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, _vp, _dp, _i64, _vp)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, _vp, _dp, _dp, _i64, _vp)
 
 
 class Transport(C.Structure):
     _fields_ = [("user", _vp), ("rank", C.c_int32), ("world", C.c_int32), ("send", SEND_FN),
-                ("recv", RECV_FN), ("allreduce_max", ALLREDUCE_FN)]
+                ("recv", RECV_FN), ("allreduce_max", ALLREDUCE_FN), ("allgather", ALLGATHER_FN)]
 
 
 # name -> (restype, argtypes); the complete export list of include/pswim_c.h
@@ -122,6 +123,10 @@ SIGNATURES = {
     "pswim_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "pswim_nccl_transport_create": (C.POINTER(Transport), [C.POINTER(C.c_uint8), _i32, _i32, C.c_int]),
     "pswim_nccl_transport_destroy": (None, [C.POINTER(Transport)]),
+    "pswim_threads_transports_create": (C.POINTER(Transport), [C.c_int32, C.POINTER(C.c_int), _i64, C.c_int32]),
+    "pswim_threads_transports_destroy": (None, [C.POINTER(Transport)]),
+    "pswim_propagate_sharded": (C.c_int, [_vp, C.POINTER(Transport), _vp, C.c_double, C.c_double, C.c_int, _i64,
+                                          C.c_double, _vp]),
     "pswim_parareal_run_threads": (C.c_int, [C.POINTER(Plan), C.POINTER(Scenario), C.POINTER(C.c_int), _i64, _i64,
                                              _dp, _dp, _dp, C.POINTER(Report)]),
     "pswim_dfma_peak": (C.c_int, [_vp, _dp, _dp]),

@@ -6,6 +6,7 @@
 // every synchronising entry point converts into the reference's exception kinds.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -212,11 +213,53 @@ int pswim_ctx::propagate_async(const double* d_in, double t0, double t1, int sch
     return PSWIM_OK;
 }
 
+// ---- space-parallel MRS (sharded targets, velocity all-gather) ------------------------
+int pswim_ctx::rhs_sharded(const pswim_transport* tr, const double* state, double t, double* u, double* w) {
+    if (!has_scenario) return fail(PSWIM_EINVAL, "rhs: context has no scenario");
+    const bool lj = rp.rods >= 2 && rp.lj_well > 0.0;  // propagators.cpp:70
+    if (lj && lj_launch(rp, state, d_lj, stream) != cudaSuccess) return fail(PSWIM_ECUDA, "lj_launch");
+    cudaError_t e = rod_loads_launch(rp, state, t, d_pos, d_f, d_n, nullptr, nullptr, lj ? d_lj : nullptr, nullptr,
+                                     nullptr, d_flags, stream);
+    if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("rod_loads_launch: ") + cudaGetErrorString(e));
+    const int64_t total = rp.rods * rp.m;
+    const MrsPlan plan = mrs_plan(total, total);
+    int rc = ensure_mrs(plan);
+    if (rc) return rc;
+    // this rank's 256-target blocks of the single-GPU plan (bitwise identical results)
+    const int world = tr->world, rank = tr->rank;
+    const int bpr = (plan.target_blocks + world - 1) / world;
+    const int tb0 = std::min(plan.target_blocks, rank * bpr), tb1 = std::min(plan.target_blocks, tb0 + bpr);
+    const int64_t shard = (int64_t)bpr * kMrsThreads;
+    if ((rc = ensure(&d_shard, &cap_shard, 6 * shard))) return rc;
+    if ((rc = ensure(&d_gather, &cap_gather, 6 * shard * world))) return rc;
+    e = mrs_launch_blocks(plan, tb0, tb1, d_pos, d_pos, d_f, d_n, rs.epsilon, rs.mu, d_shard, d_shard + 3 * shard,
+                          d_scratch, d_counters, d_flags, stream);
+    if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("mrs_launch_blocks: ") + cudaGetErrorString(e));
+    if (tr->allgather(tr->user, d_shard, d_gather, 6 * shard, stream) != 0)
+        return fail(PSWIM_ECOMM, "propagate_sharded: allgather failed");
+    e = unshard_launch(d_gather, shard, total, u, w, stream);
+    if (e != cudaSuccess) return fail(PSWIM_ECUDA, "unshard_launch");
+    return PSWIM_OK;
+}
+
+int pswim_ctx::step_sharded(const pswim_transport* tr, int scheme, const double* state, double t, double dt,
+                            double* out) {
+    int rc = rhs_sharded(tr, state, t, d_u, d_w);
+    if (rc) return rc;
+    if (scheme == PSWIM_EULER) return advance(state, d_u, d_w, dt, out);
+    rc = advance(state, d_u, d_w, 0.5 * dt, d_mid);
+    if (rc) return rc;
+    rc = rhs_sharded(tr, d_mid, t + 0.5 * dt, d_u, d_w);
+    if (rc) return rc;
+    return advance(state, d_u, d_w, dt, out);
+}
+
 pswim_ctx::~pswim_ctx() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
     harvest_timing();
-    for (double* p : {d_pos, d_f, d_n, d_u, d_w, d_lj, d_mid, d_scratch, d_metric, h_in, h_a, h_b, h_c, h_o1, h_o2})
+    for (double* p : {d_pos, d_f, d_n, d_u, d_w, d_lj, d_mid, d_scratch, d_metric, h_in, h_a, h_b, h_c, h_o1, h_o2,
+                      d_shard, d_gather})
         if (p) cudaFree(p);
     if (d_counters) cudaFree(d_counters);
     if (d_flags) cudaFree(d_flags);
@@ -440,6 +483,28 @@ int pswim_set_fused(pswim_ctx* ctx, int enable) {
     if (!ctx) return PSWIM_EINVAL;
     ctx->fused_on = enable != 0;
     return ctx->has_scenario ? fused_cluster_size(ctx->rp) : 0;
+}
+
+int pswim_propagate_sharded(pswim_ctx* ctx, const pswim_transport* tr, const double* d_in, double t0, double t1,
+                            int scheme, int64_t spi, double dtc, double* d_out) {
+    if (!ctx || !tr || !tr->allgather) return PSWIM_EINVAL;
+    if (!ctx->has_scenario) return ctx->fail(PSWIM_EINVAL, "propagate: context has no scenario");
+    int rc = ctx->use();
+    if (rc) return rc;
+    if (t1 < t0) return ctx->fail(PSWIM_EINVAL, "propagate: t1 < t0");
+    const size_t bytes = sizeof(double) * 12 * static_cast<size_t>(ctx->rp.rods * ctx->rp.m);
+    if (d_in != d_out) CK(cudaMemcpyAsync(d_out, d_in, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (t1 > t0) {
+        int64_t steps = 0;
+        double dt = 0.0;
+        if ((rc = ctx->resolve_steps(t0, t1, spi, dtc, &steps, &dt))) return rc;
+        double t = t0;
+        for (int64_t i = 0; i < steps; ++i) {
+            if ((rc = ctx->step_sharded(tr, scheme, d_out, t, dt, d_out))) return rc;
+            t += dt;  // propagators.cpp:159
+        }
+    }
+    return ctx->sync();
 }
 
 void pswim_timing_enable(pswim_ctx* ctx, int on) {

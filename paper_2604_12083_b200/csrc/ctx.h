@@ -61,4 +61,11 @@ struct pswim_ctx {
     int step(int scheme, const double* state, double t, double dt, double* out);
     int resolve_steps(double t0, double t1, int64_t spi, double dtc, int64_t* steps, double* dt);
     int propagate_async(const double* d_in, double t0, double t1, int scheme, int64_t spi, double dtc, double* d_out);
+
+    // space-parallel (sharded MRS) path
+    double* d_shard = nullptr;   // 6 S: this rank's (u, w) shard
+    double* d_gather = nullptr;  // world x 6 S
+    size_t cap_shard = 0, cap_gather = 0;
+    int rhs_sharded(const pswim_transport* tr, const double* state, double t, double* u, double* w);
+    int step_sharded(const pswim_transport* tr, int scheme, const double* state, double t, double dt, double* out);
 };

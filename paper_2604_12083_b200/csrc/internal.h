@@ -34,6 +34,13 @@ MrsPlan mrs_plan(int64_t nt, int64_t ns);
 cudaError_t mrs_launch(const MrsPlan& plan, const double* tgt, const double* src, const double* f,
                        const double* n, double eps, double mu, double* u, double* w, double* scratch,
                        unsigned* counters, unsigned* flags, cudaStream_t st);
+// Target blocks [tb0, tb1) of plan p only; outputs of target i land at index i - 256 tb0.
+cudaError_t mrs_launch_blocks(const MrsPlan& p, int tb0, int tb1, const double* tgt, const double* src,
+                              const double* f, const double* n, double eps, double mu, double* u, double* w,
+                              double* scratch, unsigned* counters, unsigned* flags, cudaStream_t st);
+// gathered = world x [u (3 S), w (3 S)] -> u, w (nt x 3), S = shard_targets
+cudaError_t unshard_launch(const double* gathered, int64_t shard_targets, int64_t nt, double* u, double* w,
+                           cudaStream_t st);
 cudaError_t h_functions_launch(const double* r, int64_t count, double eps, double* h5, cudaStream_t st);
 
 // ---- rod / propagator kernels (rod.cu) --------------------------------------------------

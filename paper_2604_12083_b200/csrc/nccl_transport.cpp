@@ -31,6 +31,7 @@ struct NcclApi {
     decltype(&ncclSend) send = nullptr;
     decltype(&ncclRecv) recv = nullptr;
     decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclAllGather) all_gather = nullptr;
 };
 
 NcclApi& api() {
@@ -56,7 +57,9 @@ NcclApi& api() {
         a.send = reinterpret_cast<decltype(a.send)>(dlsym(h, "ncclSend"));
         a.recv = reinterpret_cast<decltype(a.recv)>(dlsym(h, "ncclRecv"));
         a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
-        a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.send && a.recv && a.all_reduce;
+        a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+        a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.send && a.recv && a.all_reduce &&
+               a.all_gather;
     });
     return a;
 }
@@ -86,6 +89,14 @@ int nc_recv(void* u, double* buf, int64_t len, int32_t peer, void* st) {
 int nc_allreduce(void* u, double* buf, int64_t len, void* st) {
     auto* n = static_cast<NcclTransport*>(u);
     return api().all_reduce(buf, buf, static_cast<size_t>(len), ncclDouble, ncclMax, n->comm,
+                            static_cast<cudaStream_t>(st)) == ncclSuccess
+               ? PSWIM_OK
+               : PSWIM_ECOMM;
+}
+
+int nc_allgather(void* u, const double* send, double* recv, int64_t count, void* st) {
+    auto* n = static_cast<NcclTransport*>(u);
+    return api().all_gather(send, recv, static_cast<size_t>(count), ncclDouble, n->comm,
                             static_cast<cudaStream_t>(st)) == ncclSuccess
                ? PSWIM_OK
                : PSWIM_ECOMM;
@@ -125,6 +136,7 @@ pswim_transport* pswim_nccl_transport_create(const uint8_t* id128, int32_t rank,
     n->t.send = nc_send;
     n->t.recv = nc_recv;
     n->t.allreduce_max = nc_allreduce;
+    n->t.allgather = nc_allgather;
     return &n->t;
 }
 

@@ -1093,6 +1093,57 @@ class ThreadHub {
             return PSWIM_ECOMM;
         return PSWIM_OK;
     }
+    // Host barrier over the world (generation counted).
+    bool barrier() {
+        std::unique_lock<std::mutex> lk(mu_);
+        const long gen = bgen_;
+        if (++barrived_ == world_) {
+            barrived_ = 0;
+            ++bgen_;
+            cv_.notify_all();
+            return !aborted_;
+        }
+        cv_.wait(lk, [&] { return bgen_ != gen || aborted_; });
+        return !aborted_;
+    }
+    // recv[r * count ..] = send of rank r: stream-ordered peer copies; a second exchange of
+    // "copied" events keeps every rank's send buffer alive until all peers have read it.
+    int allgather(int rank, const double* send, double* recv, int64_t count, cudaStream_t st) {
+        cudaSetDevice(devices_[rank]);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            if (ag_send_.empty()) {
+                ag_send_.assign(world_, nullptr);
+                ag_ready_.assign(world_, nullptr);
+                ag_done_.assign(world_, nullptr);
+            }
+            if (!ag_ready_[rank]) {
+                cudaEventCreateWithFlags(&ag_ready_[rank], cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&ag_done_[rank], cudaEventDisableTiming);
+            }
+            ag_send_[rank] = send;
+        }
+        if (cudaEventRecord(ag_ready_[rank], st) != cudaSuccess) return PSWIM_ECOMM;
+        if (!barrier()) return PSWIM_ECOMM;
+        const size_t bytes = (size_t)count * sizeof(double);
+        for (int r = 0; r < world_; ++r) {
+            cudaError_t e;
+            if (r == rank) {
+                e = cudaMemcpyAsync(recv + r * count, send, bytes, cudaMemcpyDeviceToDevice, st);
+            } else {
+                e = cudaStreamWaitEvent(st, ag_ready_[r], 0);
+                if (e == cudaSuccess)
+                    e = cudaMemcpyPeerAsync(recv + r * count, devices_[rank], ag_send_[r], devices_[r], bytes, st);
+            }
+            if (e != cudaSuccess) return PSWIM_ECOMM;
+        }
+        if (cudaEventRecord(ag_done_[rank], st) != cudaSuccess) return PSWIM_ECOMM;
+        if (!barrier()) return PSWIM_ECOMM;
+        for (int r = 0; r < world_; ++r)
+            if (r != rank && cudaStreamWaitEvent(st, ag_done_[r], 0) != cudaSuccess) return PSWIM_ECOMM;
+        if (!barrier()) return PSWIM_ECOMM;  // events may be re-recorded only after all waits are queued
+        return PSWIM_OK;
+    }
     void abort() {
         std::lock_guard<std::mutex> lk(mu_);
         aborted_ = true;
@@ -1110,6 +1161,10 @@ class ThreadHub {
     long gen_ = 0;
     std::vector<double> acc_, result_;
     bool aborted_ = false;
+    int barrived_ = 0;
+    long bgen_ = 0;
+    std::vector<const double*> ag_send_;
+    std::vector<cudaEvent_t> ag_ready_, ag_done_;
 };
 
 struct HubUser {
@@ -1128,6 +1183,18 @@ int hub_allreduce(void* u, double* b, int64_t len, void* st) {
     auto* h = static_cast<HubUser*>(u);
     return h->hub->allreduce_max(h->rank, b, len, static_cast<cudaStream_t>(st));
 }
+int hub_allgather(void* u, const double* s, double* r, int64_t count, void* st) {
+    auto* h = static_cast<HubUser*>(u);
+    return h->hub->allgather(h->rank, s, r, count, static_cast<cudaStream_t>(st));
+}
+
+// Standalone in-process transports (pswim_threads_transports_create).
+struct HubBundle {
+    ThreadHub hub;
+    std::vector<HubUser> users;
+    std::vector<pswim_transport> trs;
+    HubBundle(int world, const int* devices, int64_t len, int slots) : hub(world, devices, len, slots) {}
+};
 
 }  // namespace
 }  // namespace pswim
@@ -1191,6 +1258,31 @@ int pswim_parareal_rank_host(const pswim_plan* plan, pswim_propagator_fn coarse,
     return rank_run(*plan, be, *tr, len, x0, ref_slice, state_out, rep);
 }
 
+pswim_transport* pswim_threads_transports_create(int32_t world, const int* devices, int64_t len, int32_t slots) {
+    using namespace pswim;
+    if (world < 1 || !devices) return nullptr;
+    try {
+        auto* b = new HubBundle(world, devices, len > 0 ? len : 1, slots > 0 ? slots : 1);
+        b->users.resize(world);
+        b->trs.resize(world + 1);
+        for (int p = 0; p < world; ++p) {
+            b->users[p] = HubUser{&b->hub, p};
+            b->trs[p] = pswim_transport{&b->users[p], p, world, hub_send, hub_recv, hub_allreduce, hub_allgather};
+        }
+        // trailing sentinel remembers the bundle for destroy
+        b->trs[world] = pswim_transport{b, -1, world, nullptr, nullptr, nullptr, nullptr};
+        return b->trs.data();
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+void pswim_threads_transports_destroy(pswim_transport* trs) {
+    if (!trs) return;
+    const int world = trs[0].world;
+    delete static_cast<pswim::HubBundle*>(trs[world].user);
+}
+
 int pswim_parareal_run_threads(const pswim_plan* plan, const pswim_scenario* sc, const int* devices,
                                int64_t fine_steps, int64_t coarse_steps, const double* x0, const double* reference,
                                double* states_out, pswim_report* rep) {
@@ -1215,7 +1307,7 @@ int pswim_parareal_run_threads(const pswim_plan* plan, const pswim_scenario* sc,
         Clock::time_point t_start = Clock::now();
         for (int p = 0; p < world; ++p) {
             users[p] = HubUser{&hub, p};
-            trs[p] = pswim_transport{&users[p], p, world, hub_send, hub_recv, hub_allreduce};
+            trs[p] = pswim_transport{&users[p], p, world, hub_send, hub_recv, hub_allreduce, hub_allgather};
             reps[p] = *rep;
             reps[p].eta_tilde = et[p].data();
             reps[p].eta = ea[p].data();

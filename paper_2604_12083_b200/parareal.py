@@ -293,7 +293,8 @@ class TorchTransport:
         self._send = _lib.SEND_FN(self._send_cb)
         self._recv = _lib.RECV_FN(self._recv_cb)
         self._red = _lib.ALLREDUCE_FN(self._red_cb)
-        self.c = _lib.Transport(None, rank, world, self._send, self._recv, self._red)
+        self._gather = _lib.ALLGATHER_FN(self._gather_cb)
+        self.c = _lib.Transport(None, rank, world, self._send, self._recv, self._red, self._gather)
 
     def _send_cb(self, user, buf, length, peer, stream):
         import torch
@@ -312,6 +313,18 @@ class TorchTransport:
             t = torch.empty(length, dtype=torch.float64)
             self.dist.recv(t, src=peer, group=self.group)
             np.ctypeslib.as_array(buf, shape=(length,))[:] = t.numpy()
+            return 0
+        except Exception:
+            return 7
+
+    def _gather_cb(self, user, send, recv, count, stream):
+        import torch
+
+        try:
+            t = torch.from_numpy(np.ctypeslib.as_array(send, shape=(count,)).copy())
+            out = [torch.empty(count, dtype=torch.float64) for _ in range(self.dist.get_world_size())]
+            self.dist.all_gather(out, t, group=self.group)
+            np.ctypeslib.as_array(recv, shape=(count * len(out),))[:] = torch.cat(out).numpy()
             return 0
         except Exception:
             return 7

@@ -142,3 +142,46 @@ def propagate(state, t0: float, t1: float, cfg: StepperConfig, sc: Scenario, ctx
     ctx.check(ctx.lib.pswim_propagate_host(ctx.handle, hptr(x), float(t0), float(t1), int(cfg.scheme),
                                            int(cfg.steps_per_interval), float(cfg.dt), hptr(out)))
     return out
+
+
+def propagate_sharded(state, t0: float, t1: float, cfg: StepperConfig, sc: Scenario, transport,
+                      ctx: Context | None = None):
+    """propagate with the O(N^2) MRS sharded across the ranks of `transport` (each rank its
+    256-target blocks, one (u, omega) all-gather per rhs).  Every rank passes the same full
+    state (CUDA tensor on its device); all ranks must call together.  Bitwise identical to
+    :func:`propagate` on one GPU (space-parallel MRS)."""
+    torch = _torch()
+    ctx = ctx or context_for(sc, state.device.index or 0)
+    ds = state.contiguous()
+    out = torch.empty_like(ds)
+    ctx.after_torch()
+    ctx.check(ctx.lib.pswim_propagate_sharded(ctx.handle, transport, dptr(ds), float(t0), float(t1), int(cfg.scheme),
+                                              int(cfg.steps_per_interval), float(cfg.dt), dptr(out)))
+    return out
+
+
+class ThreadTransports:
+    """`world` in-process ranks (threads) on the given devices (pswim_threads_transports_create)."""
+
+    def __init__(self, devices, len_hint: int = 1, slots: int = 4):
+        L = _lib.lib()
+        self.world = len(devices)
+        devs = (C.c_int * self.world)(*[int(d) for d in devices])
+        self.ptr = L.pswim_threads_transports_create(self.world, devs, int(len_hint), int(slots))
+        if not self.ptr:
+            raise _lib.DeviceError(6, "pswim_threads_transports_create failed")
+        self.lib = L
+
+    def __getitem__(self, rank: int):
+        return C.pointer(self.ptr[rank])
+
+    def close(self):
+        if self.ptr:
+            self.lib.pswim_threads_transports_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
