@@ -383,13 +383,42 @@ def time_steps_leg(args, world, rank, local, dev):
         t0 = time.perf_counter()
         res = pr.run_sliced_rank(plan, sc, fine_steps, coarse_steps, x0, local, transport=tr)
         wall = reduce_max(time.perf_counter() - t0, dev)
+        leg = {"metric": "simulated RK2 time-steps/s", "value": world * fine_steps / wall, "unit": "steps/s",
+               "config": {"workload": "pipelined Parareal, one slice per GPU, 64 x 256 suspension (BASELINE configs[3])",
+                          "intervals": world, "fine_rk2_steps_per_interval": fine_steps,
+                          "coarse_euler_steps_per_interval": coarse_steps, "iterations": res.report.iterations_used,
+                          "eta_tilde": res.report.eta_tilde}}
+        try:
+            leg["space_parallel"] = space_parallel_leg(sc, x0, local, dev, tr, world)
+        except Exception as e:
+            leg["space_parallel"] = {"error": f"{type(e).__name__}: {e}"}
     finally:
         _lib_destroy(tr)
-    return {"metric": "simulated RK2 time-steps/s", "value": world * fine_steps / wall, "unit": "steps/s",
-            "config": {"workload": "pipelined Parareal, one slice per GPU, 64 x 256 suspension (BASELINE configs[3])",
-                       "intervals": world, "fine_rk2_steps_per_interval": fine_steps,
-                       "coarse_euler_steps_per_interval": coarse_steps, "iterations": res.report.iterations_used,
-                       "eta_tilde": res.report.eta_tilde}}
+    return leg
+
+
+def space_parallel_leg(sc, x0, local, dev, tr, world, steps=20):
+    """Serial fine RK2 of the 64 x 256 suspension with the MRS sharded over the ranks (each
+    rank its 256-target blocks, NCCL all-gather of (u, omega) per rhs; bitwise identical to
+    one GPU): strong scaling of the time-step rate."""
+    import torch
+
+    from paper_2604_12083_b200.device import Context, dptr
+
+    ctx = Context(local, sc)
+    dx = torch.as_tensor(x0, device=dev)
+    out = torch.empty_like(dx)
+    L = ctx.lib
+    ctx.check(L.pswim_propagate_sharded(ctx.handle, tr, dptr(dx), 0.0, 2e-6, 1, 2, 0.0, dptr(out)))  # warm-up
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ctx.check(L.pswim_propagate_sharded(ctx.handle, tr, dptr(dx), 0.0, steps * 1e-6, 1, steps, 0.0, dptr(out)))
+    wall = reduce_max(time.perf_counter() - t0, dev)
+    ctx.close()
+    return {"metric": "simulated RK2 time-steps/s", "value": steps / wall, "unit": "steps/s", "scaling": "strong",
+            "config": {"workload": "serial fine RK2, 64 x 256 suspension, MRS targets sharded over the GPUs "
+                                   "(NCCL all-gather of u, omega per rhs)", "gpus": world, "steps": steps}}
 
 
 def flagellum_leg(args, local, dev):
