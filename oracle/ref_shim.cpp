@@ -391,6 +391,46 @@ int ref_serial_fine_boundaries(const pswim_scenario* s, double t0, double horizo
     })
 }
 
+// ---- config hash / trajectory files (config.cpp:191-245, io.cpp:70-106) ----
+static RunConfig run_config_of(const pswim_scenario* s, int intervals, int workers, double ratio, int max_iterations,
+                               double tolerance, int mode, int fine_steps, int coarse_steps, int stride) {
+    RunConfig c;
+    c.scenario = cfg_of(s);
+    c.intervals = intervals;
+    c.workers = workers;
+    c.ratio = ratio;
+    c.max_iterations = max_iterations;
+    c.tolerance = tolerance;
+    c.mode = mode ? parareal::Mode::pipelined : parareal::Mode::regular;
+    c.fine_steps_per_interval = fine_steps;
+    c.coarse_steps_per_interval = coarse_steps;
+    c.snapshot_stride = stride;
+    return c;
+}
+
+void ref_config_hash(const pswim_scenario* s, int intervals, int workers, double ratio, int max_iterations,
+                     double tolerance, int mode, int fine_steps, int coarse_steps, int stride, char* out17) {
+    const auto h = run_config_of(s, intervals, workers, ratio, max_iterations, tolerance, mode, fine_steps,
+                                 coarse_steps, stride)
+                       .hash();
+    std::memcpy(out17, h.c_str(), 17);
+}
+
+int ref_write_trajectory(const char* path, const pswim_scenario* s, int stride, int frames, const double* times,
+                         const double* states) {
+    GUARD({
+        const auto cfg = run_config_of(s, 8, 2, 2.0, 10, 1e-10, 1, 100, 0, stride);
+        TrajectoryWriter w(path, cfg);
+        const std::size_t len = static_cast<std::size_t>(12 * s->rod_count * s->nodes_per_rod);
+        for (int f = 0; f < frames; ++f) {
+            w.append(times[f], unpack_state(parareal::Vec(states + len * f, states + len * (f + 1)),
+                                            static_cast<std::size_t>(s->rod_count),
+                                            static_cast<std::size_t>(s->nodes_per_rod)));
+        }
+        w.close();
+    })
+}
+
 // ---- reference test oracles (tests/oracles.cpp) ----
 void ref_dense_mobility_apply(const double* nodes, int64_t n, const double* f, const double* t, double eps,
                               double mu, double* u, double* w) {

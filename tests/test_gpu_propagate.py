@@ -1,4 +1,6 @@
 """GPU parity of rhs / advance_state / step / propagate (reference propagators.cpp:38-162)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -180,3 +182,31 @@ def test_fused_stiffness_and_step_chain(gpu):
     assert np.array_equal(propagate(x, 0.0, horizon, StepperConfig(0.0, 1, 8), sc), manual)
     with pytest.raises(StiffnessError):
         propagate(x, 0.0, 50.0, StepperConfig(0.0, 1, 5), sc)
+
+
+def test_simulate_driver(gpu, oracle, tmp_path):
+    """`swim simulate` equivalent: frames every snapshot_stride, final frame vs the oracle's
+    step chain, RunRecord with the three stage timers (acceptance C7 schema)."""
+    import json
+
+    from paper_2604_12083_b200.harness import RunConfig, simulate
+    from paper_2604_12083_b200.io import read_trajectory
+    from paper_2604_12083_b200.scenario import ScenarioConfig
+    from oracle.pyoracle import Scenario as OS
+
+    cfg = RunConfig(scenario=ScenarioConfig(nodes_per_rod=11, fine_dt=0.0005, horizon=0.002), snapshot_stride=3)
+    rec = simulate(cfg, str(tmp_path), fmt="csv")
+    frames, side = read_trajectory(rec["artifacts"][0])
+    assert side["frame_count"] == len(frames) == 3  # t = 0, after 3 steps, after 4 steps
+    assert abs(frames[-1][0] - 0.002) < 1e-15
+    x = frames[0][1]
+    want = x.copy()
+    t = 0.0
+    for _ in range(4):
+        want = oracle.step(OS.make(nodes_per_rod=11), 1, want, t, 0.0005)
+        t += 0.0005
+    assert oracle.position_metric(want, frames[-1][1]) < 1e-10
+    d = json.load(open(os.path.join(str(tmp_path), f"record_simulate_{cfg.run_tag()}.json")))
+    for key in ("initialization", "velocity_computation", "triad_update"):
+        assert key in d["timings"]
+    assert d["timings"]["velocity_computation"] > 0
