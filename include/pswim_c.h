@@ -319,6 +319,26 @@ int pswim_propagate_sharded(pswim_ctx* ctx, const pswim_transport* tr, const dou
                             double t1, int scheme, int64_t steps_per_interval, double dt,
                             double* d_out);
 
+/* Fused compute + collective: the same sharded propagate with the all-gather folded into
+ * the MRS kernel's epilogue over peer memory.  Each rank creates a group on its context
+ * (exchange block [arrival counter | u,w x 2] in its HBM), shares it either as a CUDA IPC
+ * handle (64 bytes; one process per GPU, NVLink P2P) or as a raw device pointer (ranks as
+ * threads of one process), and connects to every other rank's block.  The MRS kernel then
+ * stores each target's (u, omega) into every rank's block and bumps every rank's counter with
+ * a system-scope atomic; consumers wait with an acquire spin.  Bitwise identical to
+ * pswim_propagate on one GPU. */
+typedef struct pswim_peer_group pswim_peer_group;
+pswim_peer_group* pswim_peer_group_create(pswim_ctx* ctx, int32_t rank, int32_t world);
+int pswim_peer_group_handle(pswim_peer_group* g, uint8_t* handle64);
+void* pswim_peer_group_local_base(pswim_peer_group* g);
+/* handles: world x 64 bytes (IPC, other processes) or NULL; local_bases: world device
+ * pointers (ranks of this process) or NULL.  Entry `rank` is ignored. */
+int pswim_peer_group_connect(pswim_peer_group* g, const uint8_t* handles, void* const* local_bases);
+void pswim_peer_group_destroy(pswim_peer_group* g);
+int pswim_propagate_sharded_peer(pswim_ctx* ctx, pswim_peer_group* g, const double* d_in, double t0,
+                                 double t1, int scheme, int64_t steps_per_interval, double dt,
+                                 double* d_out);
+
 /* In-process transport: `world` slice ranks as threads of one process, each on its own
  * context (any device mix), hand-offs by stream-ordered peer copies + events. */
 int pswim_parareal_run_threads(const pswim_plan* plan, const pswim_scenario* sc,

@@ -127,6 +127,13 @@ SIGNATURES = {
     "pswim_threads_transports_destroy": (None, [C.POINTER(Transport)]),
     "pswim_propagate_sharded": (C.c_int, [_vp, C.POINTER(Transport), _vp, C.c_double, C.c_double, C.c_int, _i64,
                                           C.c_double, _vp]),
+    "pswim_peer_group_create": (_vp, [_vp, _i32, _i32]),
+    "pswim_peer_group_handle": (C.c_int, [_vp, C.POINTER(C.c_uint8)]),
+    "pswim_peer_group_local_base": (_vp, [_vp]),
+    "pswim_peer_group_connect": (C.c_int, [_vp, C.POINTER(C.c_uint8), C.POINTER(_vp)]),
+    "pswim_peer_group_destroy": (None, [_vp]),
+    "pswim_propagate_sharded_peer": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_double, C.c_int, _i64, C.c_double,
+                                               _vp]),
     "pswim_parareal_run_threads": (C.c_int, [C.POINTER(Plan), C.POINTER(Scenario), C.POINTER(C.c_int), _i64, _i64,
                                              _dp, _dp, _dp, C.POINTER(Report)]),
     "pswim_dfma_peak": (C.c_int, [_vp, _dp, _dp]),

@@ -117,11 +117,12 @@ void pswim_ctx::harvest_timing() {
 
 // ---- physics on the context stream ---------------------------------------------------
 int pswim_ctx::mrs(const double* tgt, int64_t nt, const double* src, const double* f, const double* n, int64_t ns,
-                   double eps, double mu, double* u, double* w) {
+                   double eps, double mu, double* u, double* w, int pstride) {
     const MrsPlan plan = mrs_plan(nt, ns);
     int rc = ensure_mrs(plan);
     if (rc) return rc;
-    const cudaError_t e = mrs_launch(plan, tgt, src, f, n, eps, mu, u, w, d_scratch, d_counters, d_flags, stream);
+    const cudaError_t e = mrs_launch_blocks(plan, 0, plan.target_blocks, tgt, src, pstride, f, n, eps, mu, u, w,
+                                            d_scratch, d_counters, d_flags, stream);
     if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("mrs_launch: ") + cudaGetErrorString(e));
     return PSWIM_OK;
 }
@@ -135,13 +136,14 @@ int pswim_ctx::rhs(const double* state, double t, const double* ef, const double
         const cudaError_t e = lj_launch(rp, state, d_lj, stream);
         if (e != cudaSuccess) return fail(PSWIM_ECUDA, "lj_launch");
     }
-    cudaError_t e = rod_loads_launch(rp, state, t, d_pos, d_f, d_n, nullptr, nullptr, lj ? d_lj : nullptr, ef, en,
+    cudaError_t e = rod_loads_launch(rp, state, t, nullptr, d_f, d_n, nullptr, nullptr, lj ? d_lj : nullptr, ef, en,
                                      d_flags, stream);
     if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("rod_loads_launch: ") + cudaGetErrorString(e));
     stage_end();
     stage_begin(1);
     const int64_t total = rp.rods * rp.m;
-    int rc = mrs(d_pos, total, d_pos, d_f, d_n, total, rs.epsilon, rs.mu, u, w);
+    // targets = sources = node positions read in place from the packed state (stride 12)
+    int rc = mrs(state, total, state, d_f, d_n, total, rs.epsilon, rs.mu, u, w, 12);
     stage_end();
     return rc;
 }
@@ -218,7 +220,7 @@ int pswim_ctx::rhs_sharded(const pswim_transport* tr, const double* state, doubl
     if (!has_scenario) return fail(PSWIM_EINVAL, "rhs: context has no scenario");
     const bool lj = rp.rods >= 2 && rp.lj_well > 0.0;  // propagators.cpp:70
     if (lj && lj_launch(rp, state, d_lj, stream) != cudaSuccess) return fail(PSWIM_ECUDA, "lj_launch");
-    cudaError_t e = rod_loads_launch(rp, state, t, d_pos, d_f, d_n, nullptr, nullptr, lj ? d_lj : nullptr, nullptr,
+    cudaError_t e = rod_loads_launch(rp, state, t, nullptr, d_f, d_n, nullptr, nullptr, lj ? d_lj : nullptr, nullptr,
                                      nullptr, d_flags, stream);
     if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("rod_loads_launch: ") + cudaGetErrorString(e));
     const int64_t total = rp.rods * rp.m;
@@ -232,7 +234,7 @@ int pswim_ctx::rhs_sharded(const pswim_transport* tr, const double* state, doubl
     const int64_t shard = (int64_t)bpr * kMrsThreads;
     if ((rc = ensure(&d_shard, &cap_shard, 6 * shard))) return rc;
     if ((rc = ensure(&d_gather, &cap_gather, 6 * shard * world))) return rc;
-    e = mrs_launch_blocks(plan, tb0, tb1, d_pos, d_pos, d_f, d_n, rs.epsilon, rs.mu, d_shard, d_shard + 3 * shard,
+    e = mrs_launch_blocks(plan, tb0, tb1, state, state, 12, d_f, d_n, rs.epsilon, rs.mu, d_shard, d_shard + 3 * shard,
                           d_scratch, d_counters, d_flags, stream);
     if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("mrs_launch_blocks: ") + cudaGetErrorString(e));
     if (tr->allgather(tr->user, d_shard, d_gather, 6 * shard, stream) != 0)
@@ -410,7 +412,7 @@ int pswim_rod_loads(pswim_ctx* ctx, const double* d_state, double t, double* d_f
     if (!ctx->has_scenario) return ctx->fail(PSWIM_EINVAL, "rod_loads: context has no scenario");
     int rc = ctx->use();
     if (rc) return rc;
-    CK(rod_loads_launch(ctx->rp, d_state, t, ctx->d_pos, d_f, d_n, d_seg_force, d_seg_moment, nullptr, nullptr,
+    CK(rod_loads_launch(ctx->rp, d_state, t, nullptr, d_f, d_n, d_seg_force, d_seg_moment, nullptr, nullptr,
                         nullptr, ctx->d_flags, ctx->stream));
     return PSWIM_OK;
 }

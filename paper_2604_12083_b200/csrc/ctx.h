@@ -55,7 +55,7 @@ struct pswim_ctx {
     void harvest_timing();
 
     int mrs(const double* tgt, int64_t nt, const double* src, const double* f, const double* n, int64_t ns,
-            double eps, double mu, double* u, double* w);
+            double eps, double mu, double* u, double* w, int pstride = 3);
     int rhs(const double* state, double t, const double* ef, const double* en, double* u, double* w);
     int advance(const double* state, const double* u, const double* w, double dt, double* out);
     int step(int scheme, const double* state, double t, double dt, double* out);

@@ -88,7 +88,7 @@ __device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, doub
     const double ox = pos[0], oy = pos[1], oz = pos[2];
     for (int j = tid; j < N; j += bs) {
         double2 r[9];
-        if (!mrs_stage(pos, fo, no, j, ox, oy, oz, a.mc.scale, r)) fl |= kFlagNonFinite;
+        if (!mrs_stage(pos, 3, fo, no, j, ox, oy, oz, a.mc.scale, r)) fl |= kFlagNonFinite;
 #pragma unroll
         for (int q = 0; q < 9; ++q) rec[q * N + j] = r[q];
     }

@@ -27,6 +27,18 @@ struct MrsPlan {
     size_t counters = 0;
 };
 constexpr int kMrsThreads = 256;  // one target per thread
+
+// Peer epilogue of the sharded MRS: every target's final (u, w) is stored straight into each
+// rank's exchange buffer (NVLink P2P / CUDA IPC pointers, or same-device pointers), and every
+// finished 256-target block bumps each rank's arrival counter with a system-scope atomic --
+// the all-gather fused into the kernel that produces the data.
+constexpr int kMaxPeers = 16;
+struct PeerOut {
+    int world = 0;  // 0: plain local output
+    double* u[kMaxPeers];
+    double* w[kMaxPeers];
+    unsigned long long* flag[kMaxPeers];
+};
 MrsPlan mrs_plan(int64_t nt, int64_t ns);
 // Launches the all-pairs kernel (+ fused fixed-order split-source reduction).
 // d_scratch >= plan.scratch_doubles, d_counters >= plan.counters (zeroed once; the kernel
@@ -35,9 +47,12 @@ cudaError_t mrs_launch(const MrsPlan& plan, const double* tgt, const double* src
                        const double* n, double eps, double mu, double* u, double* w, double* scratch,
                        unsigned* counters, unsigned* flags, cudaStream_t st);
 // Target blocks [tb0, tb1) of plan p only; outputs of target i land at index i - 256 tb0.
-cudaError_t mrs_launch_blocks(const MrsPlan& p, int tb0, int tb1, const double* tgt, const double* src,
+cudaError_t mrs_launch_blocks(const MrsPlan& p, int tb0, int tb1, const double* tgt, const double* src, int pstride,
                               const double* f, const double* n, double eps, double mu, double* u, double* w,
-                              double* scratch, unsigned* counters, unsigned* flags, cudaStream_t st);
+                              double* scratch, unsigned* counters, unsigned* flags, cudaStream_t st,
+                              const PeerOut* d_peer = nullptr);  // device-resident PeerOut
+// Spin (one thread, acquire at system scope) until *flag >= target.
+cudaError_t peer_wait_launch(const unsigned long long* flag, unsigned long long target, cudaStream_t st);
 // gathered = world x [u (3 S), w (3 S)] -> u, w (nt x 3), S = shard_targets
 cudaError_t unshard_launch(const double* gathered, int64_t shard_targets, int64_t nt, double* u, double* w,
                            cudaStream_t st);

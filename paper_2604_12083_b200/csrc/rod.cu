@@ -52,7 +52,7 @@ rod_loads_kernel(RodArgs p, const double* __restrict__ state, double t, double* 
             f = f + ld3(extra_f + 3 * g);
             tq = tq + ld3(extra_n + 3 * g);
         }
-        st3(pos + 3 * g, ld3(xs + 12 * k));
+        if (pos) st3(pos + 3 * g, ld3(xs + 12 * k));
         st3(fo + 3 * g, f);
         st3(no + 3 * g, tq);
     }
@@ -176,7 +176,7 @@ advance_tma_kernel(const double* __restrict__ state, const double* __restrict__ 
 // (M x 96 B) arrives with one cp.async.bulk into a 2-stage ring while the previous rod is
 // processed; segments then nodes as rod_loads_kernel.
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 rod_loads_tma_kernel(RodArgs p, int64_t rods, const double* __restrict__ state, double t, double* __restrict__ pos,
                      double* __restrict__ fo, double* __restrict__ no, const double* __restrict__ lj,
                      const double* __restrict__ extra_f, const double* __restrict__ extra_n,
@@ -185,8 +185,16 @@ rod_loads_tma_kernel(RodArgs p, int64_t rods, const double* __restrict__ state, 
     const int64_t m = p.m;
     const uint32_t rod_bytes = (uint32_t)(m * 12 * sizeof(double));
     double* stage[2] = {reinterpret_cast<double*>(smem), reinterpret_cast<double*>(smem + rod_bytes)};
+    const uint32_t seg_bytes = (uint32_t)((6 * (m - 1) * sizeof(double) + 15) & ~15);
+    const uint32_t out_bytes = (uint32_t)(3 * m * sizeof(double));  // one of f / n for this rod
     double* seg = reinterpret_cast<double*>(smem + 2 * rod_bytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * rod_bytes + ((6 * (m - 1) * sizeof(double) + 15) & ~15));
+    double* outb = reinterpret_cast<double*>(smem + 2 * rod_bytes + seg_bytes);  // [f (3m), n (3m)]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * rod_bytes + seg_bytes + 2 * ((out_bytes + 15) & ~15u));
+    // outputs leave through shared memory with two bulk stores per rod when the rows are
+    // 16-byte multiples and aligned (m even), else with plain stores
+    const bool bulk_out = pos == nullptr && (out_bytes & 15) == 0 &&
+                          ((reinterpret_cast<uintptr_t>(fo) | reinterpret_cast<uintptr_t>(no)) & 15) == 0;
+    double* outn = outb + ((out_bytes + 15) & ~15u) / sizeof(double);
     if (threadIdx.x == 0) {
         mbar_init(&full[0], 1);
         mbar_init(&full[1], 1);
@@ -210,6 +218,7 @@ rod_loads_tma_kernel(RodArgs p, int64_t rods, const double* __restrict__ state, 
         mbar_wait(&full[s], (uint32_t)((k >> 1) & 1));
         for (int64_t kk = threadIdx.x; kk + 1 < m; kk += blockDim.x)
             if (!rod_segment(p, xs, kk, t, seg + 6 * kk)) fl |= kFlagDegenerate;
+        if (bulk_out && threadIdx.x == 0) bulk_wait_read<0>();  // previous rod's outputs have left outb
         __syncthreads();
         for (int64_t kk = threadIdx.x; kk < m; kk += blockDim.x) {
             d3 f, tq;
@@ -220,12 +229,23 @@ rod_loads_tma_kernel(RodArgs p, int64_t rods, const double* __restrict__ state, 
                 f = f + ld3(extra_f + 3 * g);
                 tq = tq + ld3(extra_n + 3 * g);
             }
-            st3(pos + 3 * g, ld3(xs + 12 * kk));
-            st3(fo + 3 * g, f);
-            st3(no + 3 * g, tq);
+            if (bulk_out) {
+                st3(outb + 3 * kk, f);
+                st3(outn + 3 * kk, tq);
+            } else {
+                if (pos) st3(pos + 3 * g, ld3(xs + 12 * kk));
+                st3(fo + 3 * g, f);
+                st3(no + 3 * g, tq);
+            }
         }
-        __syncthreads();  // stage s and seg are free again
+        if (bulk_out) fence_proxy_async_smem();
+        __syncthreads();  // stage s and seg are free again; outb complete
         if (threadIdx.x == 0) {
+            if (bulk_out) {
+                bulk_store(fo + 3 * m * rod, outb, out_bytes);
+                bulk_store(no + 3 * m * rod, outn, out_bytes);
+                bulk_commit();
+            }
             const int64_t rn = blockIdx.x + (k + 2) * gridDim.x;
             if (rn < rods) {
                 mbar_expect_tx(&full[s], rod_bytes);
@@ -234,6 +254,7 @@ rod_loads_tma_kernel(RodArgs p, int64_t rods, const double* __restrict__ state, 
         }
     }
     if (fl) atomicOr(flags, fl);
+    if (bulk_out && threadIdx.x == 0) bulk_wait<0>();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -407,7 +428,8 @@ cudaError_t rod_loads_launch(const RodParams& p, const double* state, double t, 
         cudaFuncSetAttribute(rod_loads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         configured = true;
     }
-    const size_t tma_smem = 2 * 96 * (size_t)p.m + ((48 * (size_t)(p.m - 1) + 15) & ~(size_t)15) + 16;
+    const size_t out_row = (24 * (size_t)p.m + 15) & ~(size_t)15;
+    const size_t tma_smem = 2 * 96 * (size_t)p.m + ((48 * (size_t)(p.m - 1) + 15) & ~(size_t)15) + 2 * out_row + 16;
     const bool aligned = (reinterpret_cast<uintptr_t>(state) & 15) == 0;
     if (seg_f == nullptr && aligned && p.rods >= 2 * 148 && tma_smem <= 200 * 1024) {
         static bool tma_configured = false;

@@ -185,3 +185,55 @@ class ThreadTransports:
             self.close()
         except Exception:
             pass
+
+
+class PeerGroup:
+    """Exchange block of one rank for the fused sharded-MRS + all-gather over peer memory
+    (pswim_peer_group_*).  Share :meth:`handle` (CUDA IPC, other processes) or :attr:`base`
+    (ranks of this process), then :meth:`connect`."""
+
+    def __init__(self, ctx: Context, rank: int, world: int):
+        self.ctx = ctx
+        self.lib = ctx.lib
+        self.rank, self.world = int(rank), int(world)
+        self.ptr = self.lib.pswim_peer_group_create(ctx.handle, self.rank, self.world)
+        if not self.ptr:
+            raise _lib.DeviceError(6, "pswim_peer_group_create failed")
+
+    def handle(self) -> bytes:
+        buf = (C.c_uint8 * 64)()
+        ctx_check = self.lib.pswim_peer_group_handle(self.ptr, buf)
+        _lib.raise_for(ctx_check, "cudaIpcGetMemHandle failed")
+        return bytes(buf)
+
+    @property
+    def base(self) -> int:
+        return self.lib.pswim_peer_group_local_base(self.ptr)
+
+    def connect(self, handles=None, bases=None) -> None:
+        if handles is not None:
+            raw = (C.c_uint8 * (64 * self.world))(*b"".join(handles))
+            rc = self.lib.pswim_peer_group_connect(self.ptr, raw, None)
+        else:
+            arr = (C.c_void_p * self.world)(*bases)
+            rc = self.lib.pswim_peer_group_connect(self.ptr, None, arr)
+        _lib.raise_for(rc, "pswim_peer_group_connect failed")
+
+    def close(self) -> None:
+        if self.ptr:
+            self.lib.pswim_peer_group_destroy(self.ptr)
+            self.ptr = None
+
+
+def propagate_sharded_peer(state, t0: float, t1: float, cfg: StepperConfig, sc: Scenario, group: PeerGroup):
+    """propagate with the sharded MRS whose all-gather is fused into the kernel epilogue over
+    peer memory; bitwise identical to :func:`propagate` on one GPU."""
+    torch = _torch()
+    ctx = group.ctx
+    ds = state.contiguous()
+    out = torch.empty_like(ds)
+    ctx.after_torch()
+    ctx.check(ctx.lib.pswim_propagate_sharded_peer(ctx.handle, group.ptr, dptr(ds), float(t0), float(t1),
+                                                   int(cfg.scheme), int(cfg.steps_per_interval), float(cfg.dt),
+                                                   dptr(out)))
+    return out

@@ -15,7 +15,7 @@ import subprocess
 import sys
 
 LIB = sys.argv[1] if len(sys.argv) > 1 else "paper_2604_12083_b200/libpswim.so"
-PAT = sys.argv[2] if len(sys.argv) > 2 else r"mrs_kernelILb1"
+PAT = sys.argv[2] if len(sys.argv) > 2 else r"mrs_kernelILb1ELb0"
 
 
 def kernel_sass(lib, pat):
