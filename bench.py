@@ -415,10 +415,37 @@ def space_parallel_leg(sc, x0, local, dev, tr, world, steps=20):
     t0 = time.perf_counter()
     ctx.check(L.pswim_propagate_sharded(ctx.handle, tr, dptr(dx), 0.0, steps * 1e-6, 1, steps, 0.0, dptr(out)))
     wall = reduce_max(time.perf_counter() - t0, dev)
+    leg = {"metric": "simulated RK2 time-steps/s", "value": steps / wall, "unit": "steps/s", "scaling": "strong",
+           "config": {"workload": "serial fine RK2, 64 x 256 suspension, MRS targets sharded over the GPUs "
+                                  "(NCCL all-gather of u, omega per rhs)", "gpus": world, "steps": steps}}
+    # the same with the all-gather fused into the MRS kernel epilogue over peer memory (IPC)
+    try:
+        import torch.distributed as dist
+
+        from paper_2604_12083_b200.propagators import PeerGroup
+
+        rank = dist.get_rank()
+        g = PeerGroup(ctx, rank, world)
+        handles = [None] * world
+        dist.all_gather_object(handles, g.handle())
+        g.connect(handles=handles)
+        barrier()
+        ctx.check(L.pswim_propagate_sharded_peer(ctx.handle, g.ptr, dptr(dx), 0.0, 2e-6, 1, 2, 0.0, dptr(out)))
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx.check(L.pswim_propagate_sharded_peer(ctx.handle, g.ptr, dptr(dx), 0.0, steps * 1e-6, 1, steps, 0.0,
+                                                 dptr(out)))
+        wall = reduce_max(time.perf_counter() - t0, dev)
+        barrier()
+        g.close()
+        leg["fused_peer_allgather"] = {"value": steps / wall, "unit": "steps/s",
+                                       "kernel": "mrs_kernel<.., kPeer> epilogue stores (u, omega) into every "
+                                                 "rank's HBM over NVLink (CUDA IPC) + system-scope arrivals"}
+    except Exception as e:
+        leg["fused_peer_allgather"] = {"error": f"{type(e).__name__}: {e}"}
     ctx.close()
-    return {"metric": "simulated RK2 time-steps/s", "value": steps / wall, "unit": "steps/s", "scaling": "strong",
-            "config": {"workload": "serial fine RK2, 64 x 256 suspension, MRS targets sharded over the GPUs "
-                                   "(NCCL all-gather of u, omega per rhs)", "gpus": world, "steps": steps}}
+    return leg
 
 
 def flagellum_leg(args, local, dev):
