@@ -278,9 +278,9 @@ def run_ours(args) -> None:
             traffic = None
     roofline = {"bound": "compute", "pipe": "FP64 FMA (CUDA cores; FP64 is not a dense contraction)",
                 "achieved": achieved, "peak": dfma_peak / 1e12, "unit": "TFLOP/s", "frac": achieved / (dfma_peak / 1e12),
-                "traffic": traffic, "kernel": "mrs_kernel<true>",
+                "traffic": traffic, "kernel": "mrs_kernel<split, variant %s>" % os.environ.get("PSWIM_MRS_TPT", "3"),
                 "flop_per_pair": FLOP_PER_PAIR, "peak_source": "DFMA microbenchmark measured in this run "
-                "(MEASURED_PEAKS.json has no FP64 entry)", "dp_instructions_per_pair": 54.5}
+                "(MEASURED_PEAKS.json has no FP64 entry)", "dp_instructions_per_pair_loop": 51}
 
     # --- secondary: simulated RK2 time-steps/s ---
     time_steps = None

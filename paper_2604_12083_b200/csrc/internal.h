@@ -26,7 +26,7 @@ struct MrsPlan {
     size_t scratch_doubles = 0;
     size_t counters = 0;
 };
-constexpr int kMrsThreads = 256;  // one target per thread
+constexpr int kMrsThreads = 256;  // targets per block (one or two per thread)
 
 // Peer epilogue of the sharded MRS: every target's final (u, w) is stored straight into each
 // rank's exchange buffer (NVLink P2P / CUDA IPC pointers, or same-device pointers), and every
@@ -40,6 +40,9 @@ struct PeerOut {
     unsigned long long* flag[kMaxPeers];
 };
 MrsPlan mrs_plan(int64_t nt, int64_t ns);
+// All-pairs kernel variant (1: 1 target/thread; 2: 2 targets/thread; 3: 2 targets/thread at
+// 3 CTAs/SM -- the default); env PSWIM_MRS_TPT overrides.
+int mrs_targets_per_thread();
 // Launches the all-pairs kernel (+ fused fixed-order split-source reduction).
 // d_scratch >= plan.scratch_doubles, d_counters >= plan.counters (zeroed once; the kernel
 // leaves them zero again).
@@ -51,6 +54,11 @@ cudaError_t mrs_launch_blocks(const MrsPlan& p, int tb0, int tb1, const double* 
                               const double* f, const double* n, double eps, double mu, double* u, double* w,
                               double* scratch, unsigned* counters, unsigned* flags, cudaStream_t st,
                               const PeerOut* d_peer = nullptr);  // device-resident PeerOut
+// Force-load (lazy module loading) every kernel a peer rank launches; call before spinning.
+void peer_preload();
+void rod_preload();
+// One arrival on every rank's counter (a rank with an empty block range, at its MRS position).
+cudaError_t peer_token_launch(const PeerOut* d_peer, cudaStream_t st);
 // Spin (one thread, acquire at system scope) until *flag >= target.
 cudaError_t peer_wait_launch(const unsigned long long* flag, unsigned long long target, cudaStream_t st);
 // gathered = world x [u (3 S), w (3 S)] -> u, w (nt x 3), S = shard_targets

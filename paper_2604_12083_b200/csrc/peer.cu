@@ -10,6 +10,7 @@
 // arrivals for this rhs.  Results are bitwise identical to the single-GPU propagate.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -72,12 +73,20 @@ int peer_rhs(pswim_ctx* ctx, pswim_peer_group* g, const double* state, double t,
     if (rc) return rc;
     const int bpr = (plan.target_blocks + g->world - 1) / g->world;
     const int tb0 = std::min(plan.target_blocks, g->rank * bpr), tb1 = std::min(plan.target_blocks, tb0 + bpr);
-    e = mrs_launch_blocks(plan, tb0, tb1, state, state, 12, ctx->d_f, ctx->d_n, ctx->rs.epsilon, ctx->rs.mu, nullptr,
-                          nullptr, ctx->d_scratch, ctx->d_counters, ctx->d_flags, ctx->stream, g->d_out[g->parity]);
+    if (tb1 > tb0)
+        e = mrs_launch_blocks(plan, tb0, tb1, state, state, 12, ctx->d_f, ctx->d_n, ctx->rs.epsilon, ctx->rs.mu,
+                              nullptr, nullptr, ctx->d_scratch, ctx->d_counters, ctx->d_flags, ctx->stream,
+                              g->d_out[g->parity]);
+    else
+        e = peer_token_launch(g->d_out[g->parity], ctx->stream);
     if (e != cudaSuccess) return ctx->fail(PSWIM_ECUDA, std::string("mrs peer launch: ") + cudaGetErrorString(e));
-    // every rank's blocks have arrived (each of the plan's target blocks signals once per rhs)
+    // every rank's blocks have arrived (each of the plan's target blocks signals once per rhs,
+    // each rank with an empty range once)
+    int idle = 0;
+    for (int r = 0; r < g->world; ++r)
+        if (std::min(plan.target_blocks, r * bpr) >= plan.target_blocks) ++idle;
     ++g->gen;
-    e = peer_wait_launch(g->flag_of(g->block), g->gen * (unsigned long long)plan.target_blocks, ctx->stream);
+    e = peer_wait_launch(g->flag_of(g->block), g->gen * (unsigned long long)(plan.target_blocks + idle), ctx->stream);
     if (e != cudaSuccess) return ctx->fail(PSWIM_ECUDA, "peer_wait");
     *u = g->u_of(g->block, g->parity);
     *w = g->w_of(g->block, g->parity);
@@ -112,6 +121,7 @@ pswim_peer_group* pswim_peer_group_create(pswim_ctx* ctx, int32_t rank, int32_t 
     g->n = ctx->rp.rods * ctx->rp.m;
     g->block_bytes = 256 + 2 * 6 * (size_t)g->n * sizeof(double);
     ctx->use();
+    pswim::peer_preload();
     if (cudaMalloc(&g->block, g->block_bytes) != cudaSuccess || cudaMemset(g->block, 0, 256) != cudaSuccess ||
         cudaDeviceSynchronize() != cudaSuccess) {
         if (g->block) cudaFree(g->block);

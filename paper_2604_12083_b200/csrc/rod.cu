@@ -455,6 +455,16 @@ cudaError_t lj_launch(const RodParams& p, const double* state, double* forces, c
     return cudaGetLastError();
 }
 
+void rod_preload() {
+    // see peer_preload (mrs.cu): load every per-step kernel before peers can spin
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, rod_loads_kernel);
+    cudaFuncGetAttributes(&a, rod_loads_tma_kernel);
+    cudaFuncGetAttributes(&a, lj_kernel);
+    cudaFuncGetAttributes(&a, advance_kernel);
+    cudaFuncGetAttributes(&a, advance_tma_kernel);
+}
+
 cudaError_t advance_launch(const RodParams& p, const double* state, const double* u, const double* w, double dt,
                            double* out, unsigned* flags, cudaStream_t st) {
     const int64_t total = p.rods * p.m;

@@ -32,3 +32,5 @@ for n in [int(a) for a in (sys.argv[1:] or ["16384", "65536", "131072"])]:
     t = min(ts)
     gp = n * n / (t * 1e-3) / 1e9
     print(f"N={n}: {t:.3f} ms  {gp:.1f} Gpair/s  {gp*103/1e3:.2f} TFLOP/s(103/pair)  frac={gp*103e9/peak:.3f}")
+    import hashlib
+    print(f"  sha1(u,w) = {hashlib.sha1(u.cpu().numpy().tobytes() + w.cpu().numpy().tobytes()).hexdigest()[:16]}")
