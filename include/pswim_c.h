@@ -149,6 +149,12 @@ int pswim_rod_loads(pswim_ctx* ctx, const double* d_state, double t, double* d_f
 /* lj_repulsion, src/rod.cpp:124-174 (raw pair forces, N x 3, before the 1/ds factor). */
 int pswim_lj_forces(pswim_ctx* ctx, const double* d_state, double* d_forces);
 
+/* LJ pair search used by pswim_lj_forces and rhs: 0 = auto (all-pairs tiles below 2048
+ * nodes, hashed cell list of side 2^(1/6) sigma above), 1 = all-pairs, 2 = cell list.
+ * Replaces the reference's O(N^2) pair loop (src/rod.cpp:146-172) without changing the pair
+ * law; the modes differ only in summation order.  Returns the previous mode. */
+int pswim_set_lj_mode(pswim_ctx* ctx, int mode);
+
 /* ---- propagators --------------------------------------------------------------------- */
 enum { PSWIM_EULER = 0, PSWIM_RK2 = 1 };
 

@@ -106,6 +106,7 @@ SIGNATURES = {
     "pswim_propagate": (C.c_int, [_vp, _vp, C.c_double, C.c_double, C.c_int, _i64, C.c_double, _vp]),
     "pswim_propagate_host": (C.c_int, [_vp, _dp, C.c_double, C.c_double, C.c_int, _i64, C.c_double, _dp]),
     "pswim_set_fused": (C.c_int, [_vp, C.c_int]),
+    "pswim_set_lj_mode": (C.c_int, [_vp, C.c_int]),
     "pswim_timing_enable": (None, [_vp, C.c_int]),
     "pswim_timing_reset": (None, [_vp]),
     "pswim_timing_snapshot": (Timing, [_vp]),

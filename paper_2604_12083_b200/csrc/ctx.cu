@@ -127,14 +127,22 @@ int pswim_ctx::mrs(const double* tgt, int64_t nt, const double* src, const doubl
     return PSWIM_OK;
 }
 
+int pswim_ctx::lj(const double* state, double* out) {
+    const int64_t total = rp.rods * rp.m;
+    const bool cells = lj_mode == 2 || (lj_mode == 0 && total >= kLjCellsMinNodes);
+    const cudaError_t e = cells ? lj_cells_launch(rp, state, out, &lj_work, stream) : lj_launch(rp, state, out, stream);
+    if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("lj: ") + cudaGetErrorString(e));
+    return PSWIM_OK;
+}
+
 int pswim_ctx::rhs(const double* state, double t, const double* ef, const double* en, double* u, double* w) {
     if (!has_scenario) return fail(PSWIM_EINVAL, "rhs: context has no scenario");
     if (sc.wall_mode == 1) return fail(PSWIM_EUNSUPPORTED_WALL, "stokes: image_wall correction is not implemented; use free_space");
     stage_begin(0);
     const bool lj = rp.rods >= 2 && rp.lj_well > 0.0;  // propagators.cpp:70
     if (lj) {
-        const cudaError_t e = lj_launch(rp, state, d_lj, stream);
-        if (e != cudaSuccess) return fail(PSWIM_ECUDA, "lj_launch");
+        const int rc = this->lj(state, d_lj);
+        if (rc) return rc;
     }
     cudaError_t e = rod_loads_launch(rp, state, t, nullptr, d_f, d_n, nullptr, nullptr, lj ? d_lj : nullptr, ef, en,
                                      d_flags, stream);
@@ -219,7 +227,10 @@ int pswim_ctx::propagate_async(const double* d_in, double t0, double t1, int sch
 int pswim_ctx::rhs_sharded(const pswim_transport* tr, const double* state, double t, double* u, double* w) {
     if (!has_scenario) return fail(PSWIM_EINVAL, "rhs: context has no scenario");
     const bool lj = rp.rods >= 2 && rp.lj_well > 0.0;  // propagators.cpp:70
-    if (lj && lj_launch(rp, state, d_lj, stream) != cudaSuccess) return fail(PSWIM_ECUDA, "lj_launch");
+    if (lj) {
+        const int rc = this->lj(state, d_lj);
+        if (rc) return rc;
+    }
     cudaError_t e = rod_loads_launch(rp, state, t, nullptr, d_f, d_n, nullptr, nullptr, lj ? d_lj : nullptr, nullptr,
                                      nullptr, d_flags, stream);
     if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("rod_loads_launch: ") + cudaGetErrorString(e));
@@ -264,6 +275,7 @@ pswim_ctx::~pswim_ctx() {
                       d_shard, d_gather})
         if (p) cudaFree(p);
     if (d_counters) cudaFree(d_counters);
+    lj_work.release();
     if (d_flags) cudaFree(d_flags);
     if (h_flags) cudaFreeHost(h_flags);
     if (stream) cudaStreamDestroy(stream);
@@ -281,6 +293,7 @@ pswim_ctx* pswim_create(int device, const pswim_scenario* sc, int stream_priorit
         delete ctx;
         return nullptr;
     }
+    pswim::preload_kernels(device);
     if (cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, stream_priority) != cudaSuccess ||
         cudaMalloc(&ctx->d_flags, sizeof(unsigned)) != cudaSuccess ||
         cudaMallocHost(&ctx->h_flags, sizeof(unsigned)) != cudaSuccess ||
@@ -311,6 +324,14 @@ pswim_ctx* pswim_create(int device, const pswim_scenario* sc, int stream_priorit
         if (ctx->ensure_mrs(plan)) {
             delete ctx;
             return nullptr;
+        }
+        if (ctx->rp.rods >= 2 && ctx->rp.lj_well > 0.0 && ctx->rs.total_nodes >= kLjCellsMinNodes) {
+            // cell-list workspace + one warm-up pass (loads its sort kernels, see preload_kernels)
+            if (cudaMemsetAsync(ctx->d_mid, 0, sizeof(double) * 4 * n3, ctx->stream) != cudaSuccess ||
+                lj_cells_launch(ctx->rp, ctx->d_mid, ctx->d_lj, &ctx->lj_work, ctx->stream) != cudaSuccess) {
+                delete ctx;
+                return nullptr;
+            }
         }
     }
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
@@ -426,7 +447,7 @@ int pswim_lj_forces(pswim_ctx* ctx, const double* d_state, double* d_forces) {
         CK(cudaMemsetAsync(d_forces, 0, sizeof(double) * 3 * ctx->rp.rods * ctx->rp.m, ctx->stream));
         return PSWIM_OK;
     }
-    CK(lj_launch(ctx->rp, d_state, d_forces, ctx->stream));
+    return ctx->lj(d_state, d_forces);
     return PSWIM_OK;
 }
 
@@ -479,6 +500,13 @@ int pswim_propagate_host(pswim_ctx* ctx, const double* h_in, double t0, double t
     if (rc) return rc;
     CK(cudaMemcpyAsync(h_out, ctx->h_in, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     return ctx->sync();
+}
+
+int pswim_set_lj_mode(pswim_ctx* ctx, int mode) {
+    if (!ctx || mode < 0 || mode > 2) return -PSWIM_EINVAL;
+    const int prev = ctx->lj_mode;
+    ctx->lj_mode = mode;
+    return prev;
 }
 
 int pswim_set_fused(pswim_ctx* ctx, int enable) {

@@ -40,6 +40,8 @@ struct pswim_ctx {
     };
     bool timing_on = false;
     bool fused_on = true;  // whole-interval fused kernel for N <= 256 (fused.cu)
+    int lj_mode = 0;       // 0 auto (all-pairs below kLjCellsMinNodes), 1 all-pairs, 2 cell list
+    pswim::LjWork lj_work;
     std::vector<TimedStage> open_stages, done_stages;
     double stage_seconds[3] = {0, 0, 0};
 
@@ -56,6 +58,7 @@ struct pswim_ctx {
 
     int mrs(const double* tgt, int64_t nt, const double* src, const double* f, const double* n, int64_t ns,
             double eps, double mu, double* u, double* w, int pstride = 3);
+    int lj(const double* state, double* out);  // lj_repulsion, rod.cpp:124-174
     int rhs(const double* state, double t, const double* ef, const double* en, double* u, double* w);
     int advance(const double* state, const double* u, const double* w, double dt, double* out);
     int step(int scheme, const double* state, double t, double dt, double* out);

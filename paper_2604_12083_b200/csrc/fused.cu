@@ -66,8 +66,11 @@ __device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, doub
         for (int i = tid; i < N; i += bs) {
             double fx = 0, fy = 0, fz = 0;
             const double xi = xs[12 * i], yi = xs[12 * i + 1], zi = xs[12 * i + 2];
-            for (int j = 0; j < N; ++j)
-                lj_pair(a.lj, i, j, xi - xs[12 * j], yi - xs[12 * j + 1], zi - xs[12 * j + 2], fx, fy, fz);
+            const int ri = i / m, ki = i - ri * m;
+            for (int rj = 0, j = 0; rj < a.lj.rods; ++rj)
+                for (int kj = 0; kj < m; ++kj, ++j)
+                    lj_pair(a.lj, ri, ki, rj, kj, xi - xs[12 * j], yi - xs[12 * j + 1], zi - xs[12 * j + 2], fx, fy,
+                            fz);
             ljf[3 * i] = fx;
             ljf[3 * i + 1] = fy;
             ljf[3 * i + 2] = fz;
@@ -224,6 +227,14 @@ int fused_cluster_size(const RodParams& p) {
     const int64_t doubles = 24 * n + 12 * n + 6 * p.rods * (p.m - 1) + 18 * n + plan.chunks * tpc * 6 + 12 * n + 16;
     if (doubles * 8 > 220 * 1024) return 0;
     return cs;
+}
+
+void fused_preload() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, fused_kernel<1>);
+    cudaFuncGetAttributes(&a, fused_kernel<2>);
+    cudaFuncGetAttributes(&a, fused_kernel<4>);
+    cudaFuncGetAttributes(&a, fused_kernel<8>);
 }
 
 cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t steps, double t0, double dt, int scheme,

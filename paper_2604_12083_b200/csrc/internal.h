@@ -57,6 +57,11 @@ cudaError_t mrs_launch_blocks(const MrsPlan& p, int tb0, int tb1, const double* 
 // Force-load (lazy module loading) every kernel a peer rank launches; call before spinning.
 void peer_preload();
 void rod_preload();
+void fused_preload();
+// Every kernel of the library is loaded on `device` before a context can launch anything:
+// CUDA lazy module loading may synchronise the context on a kernel's first launch, which
+// deadlocks against a spinning peer / NCCL kernel in another stream of this process.
+void preload_kernels(int device);
 // One arrival on every rank's counter (a rank with an empty block range, at its MRS position).
 cudaError_t peer_token_launch(const PeerOut* d_peer, cudaStream_t st);
 // Spin (one thread, acquire at system scope) until *flag >= target.
@@ -82,6 +87,22 @@ cudaError_t rod_loads_launch(const RodParams& p, const double* state, double t, 
                              double* n, double* seg_f, double* seg_n, const double* lj, const double* extra_f,
                              const double* extra_n, unsigned* flags, cudaStream_t st);
 cudaError_t lj_launch(const RodParams& p, const double* state, double* forces, cudaStream_t st);
+// Hashed cell-list LJ (lj_cells.cu): workspace grown on demand, owned by the context.
+struct LjWork {
+    int64_t cap_nodes = 0, cap_buckets = 0;
+    unsigned *key = nullptr, *key_sorted = nullptr;
+    int *idx = nullptr, *idx_sorted = nullptr, *cell_start = nullptr, *cell_end = nullptr;
+    double* pos = nullptr;
+    int2* rk = nullptr;  // (rod, node-in-rod) per sorted entry
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    void release();
+};
+int lj_buckets(int64_t n);
+cudaError_t lj_cells_launch(const RodParams& p, const double* state, double* forces, LjWork* w, cudaStream_t st);
+void lj_cells_preload();
+// all-pairs kernel below this many nodes in LJ auto mode, cell list above
+constexpr int64_t kLjCellsMinNodes = 2048;
 cudaError_t advance_launch(const RodParams& p, const double* state, const double* u, const double* w, double dt,
                            double* out, unsigned* flags, cudaStream_t st);
 cudaError_t sqrt_batched_launch(const double* r9, int64_t count, double* s9, cudaStream_t st);

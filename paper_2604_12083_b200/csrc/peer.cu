@@ -63,7 +63,10 @@ namespace pswim {
 int peer_rhs(pswim_ctx* ctx, pswim_peer_group* g, const double* state, double t, double** u, double** w) {
     const RodParams& rp = ctx->rp;
     const bool lj = rp.rods >= 2 && rp.lj_well > 0.0;  // propagators.cpp:70
-    if (lj && lj_launch(rp, state, ctx->d_lj, ctx->stream) != cudaSuccess) return ctx->fail(PSWIM_ECUDA, "lj_launch");
+    if (lj) {
+        const int rc = ctx->lj(state, ctx->d_lj);
+        if (rc) return rc;
+    }
     cudaError_t e = rod_loads_launch(rp, state, t, nullptr, ctx->d_f, ctx->d_n, nullptr, nullptr,
                                      lj ? ctx->d_lj : nullptr, nullptr, nullptr, ctx->d_flags, ctx->stream);
     if (e != cudaSuccess) return ctx->fail(PSWIM_ECUDA, std::string("rod_loads_launch: ") + cudaGetErrorString(e));

@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "kernels.cuh"
 #include "tma.cuh"
@@ -69,27 +71,32 @@ constexpr int kLjTile = 256;
 __global__ void __launch_bounds__(256)
 lj_kernel(const double* __restrict__ state, LjArgs a, double* __restrict__ out) {
     __shared__ double sx[kLjTile], sy[kLjTile], sz[kLjTile];
-    const int64_t total = a.rods * a.m;
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t il = i < total ? i : total - 1;
-    const double xi = state[12 * il], yi = state[12 * il + 1], zi = state[12 * il + 2];
+    __shared__ int srod[kLjTile], sk[kLjTile];
+    const int total = a.rods * a.m;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int il = i < total ? i : total - 1;
+    const int ri = il / a.m, ki = il - ri * a.m;
+    const double xi = state[12 * (int64_t)il], yi = state[12 * (int64_t)il + 1], zi = state[12 * (int64_t)il + 2];
     double fx = 0, fy = 0, fz = 0;
-    for (int64_t jt = 0; jt < total; jt += kLjTile) {
-        const int cnt = (total - jt) < kLjTile ? (int)(total - jt) : kLjTile;
+    for (int jt = 0; jt < total; jt += kLjTile) {
+        const int cnt = (total - jt) < kLjTile ? total - jt : kLjTile;
         __syncthreads();
         if (threadIdx.x < cnt) {
-            const int64_t j = jt + threadIdx.x;
-            sx[threadIdx.x] = state[12 * j];
-            sy[threadIdx.x] = state[12 * j + 1];
-            sz[threadIdx.x] = state[12 * j + 2];
+            const int j = jt + threadIdx.x;
+            sx[threadIdx.x] = state[12 * (int64_t)j];
+            sy[threadIdx.x] = state[12 * (int64_t)j + 1];
+            sz[threadIdx.x] = state[12 * (int64_t)j + 2];
+            srod[threadIdx.x] = j / a.m;
+            sk[threadIdx.x] = j - (j / a.m) * a.m;
         }
         __syncthreads();
-        for (int jj = 0; jj < cnt; ++jj) lj_pair(a, il, jt + jj, xi - sx[jj], yi - sy[jj], zi - sz[jj], fx, fy, fz);
+        for (int jj = 0; jj < cnt; ++jj)
+            lj_pair(a, ri, ki, srod[jj], sk[jj], xi - sx[jj], yi - sy[jj], zi - sz[jj], fx, fy, fz);
     }
     if (i < total) {
-        out[3 * i] = fx;
-        out[3 * i + 1] = fy;
-        out[3 * i + 2] = fz;
+        out[3 * (int64_t)i] = fx;
+        out[3 * (int64_t)i + 1] = fy;
+        out[3 * (int64_t)i + 2] = fz;
     }
 }
 
@@ -481,6 +488,17 @@ cudaError_t rod_loads_launch(const RodParams& p, const double* state, double t, 
     return cudaGetLastError();
 }
 
+void preload_kernels(int device) {
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (std::find(done.begin(), done.end(), device) != done.end()) return;
+    peer_preload();  // MRS + peer kernels, rod kernels
+    lj_cells_preload();
+    fused_preload();
+    done.push_back(device);
+}
+
 cudaError_t lj_launch(const RodParams& p, const double* state, double* forces, cudaStream_t st) {
     const int64_t total = p.rods * p.m;
     lj_kernel<<<grid_for(total, 256), 256, 0, st>>>(state, lj_args(p), forces);
@@ -493,6 +511,10 @@ void rod_preload() {
     cudaFuncGetAttributes(&a, rod_loads_kernel);
     cudaFuncGetAttributes(&a, rod_loads_wtma_kernel<kRodStages>);
     cudaFuncGetAttributes(&a, lj_kernel);
+    cudaFuncGetAttributes(&a, sqrt_tma_kernel);
+    cudaFuncGetAttributes(&a, sqrt_plain_kernel);
+    cudaFuncGetAttributes(&a, metric_kernel);
+    cudaFuncGetAttributes(&a, correct_kernel);
     cudaFuncGetAttributes(&a, advance_kernel);
     cudaFuncGetAttributes(&a, advance_tma_kernel);
 }
