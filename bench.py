@@ -299,6 +299,14 @@ def run_ours(args) -> None:
         hbm = hbm_kernels(local)
         for v in hbm.values():
             v["frac_of_measured_hbm"] = v["GB_per_s"] / _hbm_peak()
+        try:
+            from probe_lj import lj_times
+
+            hbm["lj_repulsion"] = {"workload": "LJ pair forces (lj_well_depth = 0.01, grid suspensions perturbed "
+                                               "by 0.5 sigma into contact), ms per evaluation",
+                                   **lj_times(local)}
+        except Exception as e:
+            hbm["lj_repulsion"] = {"error": f"{type(e).__name__}: {e}"}
 
     # --- CPU baseline (reference, host cores) ---
     cpu = None
@@ -369,6 +377,18 @@ def time_steps_leg(args, world, rank, local, dev):
         leg = {"metric": "simulated RK2 time-steps/s", "value": steps / sec, "unit": "steps/s",
                "config": {"workload": "serial fine RK2, 64 x 256 suspension, eps=0.08, dt=1e-6 (BASELINE configs[2])",
                           "steps": steps}, "gpu_launches_per_step": 6}
+        if not args.no_cpu:
+            from oracle.pyoracle import LIB_PATHS, Oracle, Scenario as OS
+
+            if os.path.exists(LIB_PATHS["ref"]):
+                ref = Oracle("ref")
+                osc = OS.make(rod_count=64, nodes_per_rod=256, epsilon=0.08)
+                t0 = time.perf_counter()
+                ref.propagate(osc, x0, 0.0, 2e-6, 1, steps=2)
+                cpu = 2 / (time.perf_counter() - t0)
+                leg["cpu_baseline"] = {"value": cpu, "unit": "steps/s", "cores": ref.max_threads_(),
+                                       "kind": "reference",
+                                       "sample": "2 RK2 steps of the same suspension (reference propagate, OpenMP)"}
         leg["flagellum"] = flagellum_leg(args, local, dev)
         return leg
     # N > 1: one Parareal slice per GPU, NCCL hand-offs
@@ -392,9 +412,47 @@ def time_steps_leg(args, world, rank, local, dev):
             leg["space_parallel"] = space_parallel_leg(sc, x0, local, dev, tr, world)
         except Exception as e:
             leg["space_parallel"] = {"error": f"{type(e).__name__}: {e}"}
+        if world >= 4 and world % 2 == 0:
+            try:
+                leg["hybrid_space_time"] = hybrid_leg(args, sc, x0, local, dev, world, members=2)
+            except Exception as e:
+                leg["hybrid_space_time"] = {"error": f"{type(e).__name__}: {e}"}
     finally:
         _lib_destroy(tr)
     return leg
+
+
+def hybrid_leg(args, sc, x0, local, dev, world, members):
+    """Hybrid space x time: world / members Parareal slices, each propagated by a space group
+    of `members` GPUs that shards every rhs's MRS (NCCL all-gather); slice hand-offs between
+    same-index members."""
+    import torch.distributed as dist
+
+    from paper_2604_12083_b200 import parareal as pr
+
+    rank = dist.get_rank()
+    slices = world // members
+    tg, sg = pr.hybrid_groups(world, members)
+    groups = tg + sg + sg  # time, space (coarse), space (fine): every rank creates them in this order
+    trs = pr.nccl_group_transports(local, groups)
+    q, p = rank % members, rank // members
+    t_tr, c_tr, f_tr = trs[q], trs[len(tg) + p], trs[len(tg) + len(sg) + p]
+    fine_steps, coarse_steps = args.fine_steps, max(1, args.fine_steps // 10)
+    plan = pr.ParallelPlan(t0=0.0, horizon=slices * fine_steps * 1e-6, intervals=slices, workers=slices,
+                           max_iterations=args.parareal_iters, tolerance=1e-300, mode=pr.PIPELINED)
+    try:
+        pr.run_sliced_rank(plan, sc, fine_steps, coarse_steps, x0, local, transport=t_tr, space=(c_tr, f_tr))
+        barrier()
+        t0 = time.perf_counter()
+        res = pr.run_sliced_rank(plan, sc, fine_steps, coarse_steps, x0, local, transport=t_tr, space=(c_tr, f_tr))
+        wall = reduce_max(time.perf_counter() - t0, dev)
+    finally:
+        for tr in trs.values():
+            _lib_destroy(tr)
+    return {"metric": "simulated RK2 time-steps/s", "value": slices * fine_steps / wall, "unit": "steps/s",
+            "config": {"workload": f"pipelined Parareal, {slices} slices x {members} GPUs per slice (MRS sharded "
+                                   "inside each slice), 64 x 256 suspension", "fine_rk2_steps_per_interval": fine_steps,
+                       "coarse_euler_steps_per_interval": coarse_steps, "iterations": res.report.iterations_used}}
 
 
 def space_parallel_leg(sc, x0, local, dev, tr, world, steps=20):

@@ -184,6 +184,14 @@ int pswim_propagate(pswim_ctx* ctx, const double* d_in, double t0, double t1, in
  * the cluster size used for the context's scenario (0 = not eligible). */
 int pswim_set_fused(pswim_ctx* ctx, int enable);
 
+/* The fused small-system propagate (pswim_set_fused) with its in-kernel phase timer on:
+ * clock64 cycles of cluster rank 0 spent in 7 phases summed over all steps -- segment loads
+ * (+LJ), nodal loads, MRS source staging, MRS pairs, chunk reduction + velocity push,
+ * cluster barrier, advance (the reference's stage timers, propagators.hpp:55-65, for a path
+ * that is a single kernel).  PSWIM_EINVAL when the scenario is not fused-eligible. */
+int pswim_fused_profile(pswim_ctx* ctx, const double* d_in, double t0, double t1, int scheme,
+                        int64_t steps_per_interval, double* d_out, uint64_t* h_cycles7);
+
 /* Host-buffer propagate (e2e boundary: H2D, propagate, D2H). */
 int pswim_propagate_host(pswim_ctx* ctx, const double* h_in, double t0, double t1, int scheme,
                          int64_t steps_per_interval, double dt, double* h_out);
@@ -293,6 +301,19 @@ int pswim_parareal_rank_gpu(const pswim_plan* plan, const pswim_scenario* sc, in
                             const pswim_transport* tr, int64_t fine_steps, int64_t coarse_steps,
                             const double* h_x0, const double* h_reference_slice /* or NULL */,
                             double* h_state_out, pswim_report* report);
+
+/* Hybrid space x time: the rank is member q of the space group of slice
+ * p.  time_tr connects the q-th members of all slices (rank = slice, world = intervals) and
+ * carries the slice hand-offs and the metric allreduce exactly as pswim_parareal_rank_gpu;
+ * space_coarse / space_fine (same group, rank = q, one per stream) all-gather (u, omega) of
+ * the MRS sharded over the group inside every coarse / fine rhs.  Every member of a slice
+ * computes the same values, bitwise equal to the unsharded rank driver. */
+int pswim_parareal_rank_gpu_hybrid(const pswim_plan* plan, const pswim_scenario* sc, int device,
+                                   const pswim_transport* time_tr, const pswim_transport* space_coarse,
+                                   const pswim_transport* space_fine, int64_t fine_steps,
+                                   int64_t coarse_steps, const double* h_x0,
+                                   const double* h_reference_slice /* or NULL */, double* h_state_out,
+                                   pswim_report* report);
 
 /* Host form of the same rank driver (host propagators + host transport): used by the
  * world_size>1 CPU tests of the rank logic. */

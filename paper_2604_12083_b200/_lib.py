@@ -107,6 +107,8 @@ SIGNATURES = {
     "pswim_propagate_host": (C.c_int, [_vp, _dp, C.c_double, C.c_double, C.c_int, _i64, C.c_double, _dp]),
     "pswim_set_fused": (C.c_int, [_vp, C.c_int]),
     "pswim_set_lj_mode": (C.c_int, [_vp, C.c_int]),
+    "pswim_fused_profile": (C.c_int, [_vp, _vp, C.c_double, C.c_double, C.c_int, C.c_int64, _vp,
+                                      C.POINTER(C.c_uint64)]),
     "pswim_timing_enable": (None, [_vp, C.c_int]),
     "pswim_timing_reset": (None, [_vp]),
     "pswim_timing_snapshot": (Timing, [_vp]),
@@ -119,6 +121,9 @@ SIGNATURES = {
                                          C.POINTER(Report), C.POINTER(TraceEvent), _i64, C.POINTER(_i64)]),
     "pswim_parareal_rank_gpu": (C.c_int, [C.POINTER(Plan), C.POINTER(Scenario), C.c_int, C.POINTER(Transport), _i64, _i64,
                                           _dp, _dp, _dp, C.POINTER(Report)]),
+    "pswim_parareal_rank_gpu_hybrid": (C.c_int, [C.POINTER(Plan), C.POINTER(Scenario), C.c_int, C.POINTER(Transport),
+                                                 C.POINTER(Transport), C.POINTER(Transport), _i64, _i64, _dp, _dp,
+                                                 _dp, C.POINTER(Report)]),
     "pswim_parareal_rank_host": (C.c_int, [C.POINTER(Plan), PROPAGATOR_FN, _vp, PROPAGATOR_FN, _vp,
                                            C.POINTER(Transport), _dp, _i64, _i32, _i32, _dp, _dp, C.POINTER(Report)]),
     "pswim_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),

@@ -195,7 +195,7 @@ int pswim_ctx::resolve_steps(double t0, double t1, int64_t steps_per_interval, d
 }
 
 int pswim_ctx::propagate_async(const double* d_in, double t0, double t1, int scheme, int64_t spi, double dtc,
-                               double* d_out) {
+                               double* d_out, const pswim_transport* space) {
     if (!has_scenario) return fail(PSWIM_EINVAL, "propagate: context has no scenario");
     const size_t bytes = sizeof(double) * 12 * static_cast<size_t>(rp.rods * rp.m);
     if (t1 < t0) return fail(PSWIM_EINVAL, "propagate: t1 < t0");
@@ -208,6 +208,16 @@ int pswim_ctx::propagate_async(const double* d_in, double t0, double t1, int sch
     double dt = 0.0;
     int rc = resolve_steps(t0, t1, spi, dtc, &steps, &dt);
     if (rc) return rc;
+    if (space && space->world > 1) {
+        // space-parallel: the MRS targets of every rhs sharded over the space group
+        double t = t0;
+        for (int64_t i = 0; i < steps; ++i) {
+            rc = step_sharded(space, scheme, d_out, t, dt, d_out);
+            if (rc) return rc;
+            t += dt;  // propagators.cpp:159
+        }
+        return PSWIM_OK;
+    }
     if (fused_on && !timing_on && fused_cluster_size(rp) > 0) {
         // the whole interval in one launch, bitwise identical to the loop below
         const cudaError_t e = fused_propagate_launch(rp, d_out, steps, t0, dt, scheme, d_flags, stream);
@@ -500,6 +510,30 @@ int pswim_propagate_host(pswim_ctx* ctx, const double* h_in, double t0, double t
     if (rc) return rc;
     CK(cudaMemcpyAsync(h_out, ctx->h_in, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     return ctx->sync();
+}
+
+int pswim_fused_profile(pswim_ctx* ctx, const double* d_in, double t0, double t1, int scheme, int64_t spi,
+                        double* d_out, uint64_t* h_cycles7) {
+    if (!ctx || !h_cycles7) return PSWIM_EINVAL;
+    if (!ctx->has_scenario || fused_cluster_size(ctx->rp) == 0)
+        return ctx->fail(PSWIM_EINVAL, "fused_profile: scenario not eligible for the fused path");
+    int rc = ctx->use();
+    if (rc) return rc;
+    if (t1 < t0) return ctx->fail(PSWIM_EINVAL, "propagate: t1 < t0");
+    int64_t steps = 0;
+    double dt = 0.0;
+    if ((rc = ctx->resolve_steps(t0, t1, spi, 0.0, &steps, &dt))) return rc;
+    const size_t bytes = sizeof(double) * 12 * static_cast<size_t>(ctx->rp.rods * ctx->rp.m);
+    unsigned long long* prof = nullptr;
+    CK(cudaMalloc(&prof, sizeof(unsigned long long) * kFusedPhases));
+    CK(cudaMemsetAsync(prof, 0, sizeof(unsigned long long) * kFusedPhases, ctx->stream));
+    if (d_in != d_out) CK(cudaMemcpyAsync(d_out, d_in, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(fused_propagate_launch(ctx->rp, d_out, steps, t0, dt, scheme, ctx->d_flags, ctx->stream, prof));
+    CK(cudaMemcpyAsync(h_cycles7, prof, sizeof(unsigned long long) * kFusedPhases, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    rc = ctx->sync();
+    cudaFree(prof);
+    return rc;
 }
 
 int pswim_set_lj_mode(pswim_ctx* ctx, int mode) {

@@ -63,7 +63,9 @@ struct pswim_ctx {
     int advance(const double* state, const double* u, const double* w, double dt, double* out);
     int step(int scheme, const double* state, double t, double dt, double* out);
     int resolve_steps(double t0, double t1, int64_t spi, double dtc, int64_t* steps, double* dt);
-    int propagate_async(const double* d_in, double t0, double t1, int scheme, int64_t spi, double dtc, double* d_out);
+    // space: optional transport of a space group -> every rhs with the MRS sharded over it
+    int propagate_async(const double* d_in, double t0, double t1, int scheme, int64_t spi, double dtc, double* d_out,
+                        const pswim_transport* space = nullptr);
 
     // space-parallel (sharded MRS) path
     double* d_shard = nullptr;   // 6 S: this rank's (u, w) shard

@@ -36,6 +36,23 @@ struct FusedArgs {
     // shared-memory offsets (doubles)
     int off_x, off_xm, off_pos, off_f, off_n, off_seg, off_lj, off_rec, off_part, off_vel;
     int part_stride;  // unused (kept for layout clarity)
+    unsigned long long* prof;  // kFusedPhases clock64 counters (CTA 0, thread 0), nullptr = off
+};
+
+// In-kernel phase timer: clock64 deltas between the CTA barriers that end each phase, as seen
+// by thread 0 of cluster rank 0 (the stage timers of propagators.hpp:55-65 for a path that is
+// one kernel).  Phases: 0 segment loads (+LJ), 1 nodal loads, 2 MRS source staging, 3 MRS
+// pairs, 4 chunk reduction + DSMEM velocity push, 5 cluster barrier, 6 advance.
+struct PhaseClock {
+    unsigned long long* prof;
+    long long t;
+    __device__ __forceinline__ void mark(int phase) {
+        if (prof) {
+            const long long c = clock64();
+            prof[phase] += (unsigned long long)(c - t);
+            t = c;
+        }
+    }
 };
 
 template <int CS>
@@ -49,7 +66,8 @@ __device__ __forceinline__ void cluster_barrier() {
 
 // rhs (propagators.cpp:38-91) of the state `xs` at time t into vel[6 n] = (u, w) per node.
 template <int CS>
-__device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, double t, double* vel, unsigned& fl) {
+__device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, double t, double* vel, unsigned& fl,
+                          PhaseClock& pc) {
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n, m = a.m, nseg = a.rods * (m - 1);
     double* pos = sm + a.off_pos;
     double* fo = sm + a.off_f;
@@ -77,6 +95,7 @@ __device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, doub
         }
     }
     __syncthreads();
+    pc.mark(0);
     for (int g = tid; g < N; g += bs) {
         const int r = g / m, k = g % m;
         d3 f, tq;
@@ -87,6 +106,7 @@ __device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, doub
         st3(no + 3 * g, tq);
     }
     __syncthreads();
+    pc.mark(1);
     // stage every source relative to node 0 (the single target block's origin in mrs.cu)
     const double ox = pos[0], oy = pos[1], oz = pos[2];
     for (int j = tid; j < N; j += bs) {
@@ -96,6 +116,7 @@ __device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, doub
         for (int q = 0; q < 9; ++q) rec[q * N + j] = r[q];
     }
     __syncthreads();
+    pc.mark(2);
     // MRS: this CTA owns targets [i0, i1); items (target, source chunk) computed here, the
     // chunk partials reduced locally in fixed order (mrs.cu's last-CTA reduction), and each
     // target's 6 velocities pushed to every CTA of the cluster through DSMEM.
@@ -120,6 +141,7 @@ __device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, doub
         for (int q = 0; q < 6; ++q) lpart[(c * tpc + il) * 6 + q] = out[q];
     }
     __syncthreads();
+    pc.mark(3);
     for (int il = tid; il < nloc; il += bs) {
         double sum[6];
 #pragma unroll
@@ -141,7 +163,10 @@ __device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, doub
             for (int q = 0; q < 6; ++q) vel[6 * i + q] = sum[q];
         }
     }
+    if (a.prof) __syncthreads();  // phase timer only: end of the push as one CTA-wide instant
+    pc.mark(4);
     cluster_barrier<CS>();
+    pc.mark(5);
 }
 
 template <int CS>
@@ -157,32 +182,36 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
     unsigned fl = 0;
     int parity = 0;
     double t = t0;
+    const int crank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
+    PhaseClock pc{(a.prof && tid == 0 && crank == 0) ? a.prof : nullptr, clock64()};
     // velocities are double-buffered: a CTA that runs ahead pushes the next rhs into the
     // other buffer while slower CTAs still read this one (the next cluster barrier orders it)
     for (int64_t s = 0; s < steps; ++s) {
         double* vel = sm + a.off_vel + parity * 6 * N;
-        fused_rhs<CS>(a, sm, x, t, vel, fl);
+        fused_rhs<CS>(a, sm, x, t, vel, fl, pc);
         parity ^= 1;
         if (scheme == PSWIM_EULER) {
             for (int i = tid; i < N; i += bs)
                 fl |= advance_node(x + 12 * i, vel + 6 * i, vel + 6 * i + 3, dt, a.max_disp, x + 12 * i);
             __syncthreads();
+            pc.mark(6);
         } else {
             // step_rk2, propagators.cpp:130-133
             for (int i = tid; i < N; i += bs)
                 fl |= advance_node(x + 12 * i, vel + 6 * i, vel + 6 * i + 3, 0.5 * dt, a.max_disp, xm + 12 * i);
             __syncthreads();
+            pc.mark(6);
             vel = sm + a.off_vel + parity * 6 * N;
-            fused_rhs<CS>(a, sm, xm, t + 0.5 * dt, vel, fl);
+            fused_rhs<CS>(a, sm, xm, t + 0.5 * dt, vel, fl, pc);
             parity ^= 1;
             for (int i = tid; i < N; i += bs)
                 fl |= advance_node(x + 12 * i, vel + 6 * i, vel + 6 * i + 3, dt, a.max_disp, x + 12 * i);
             __syncthreads();
+            pc.mark(6);
         }
         t += dt;  // propagators.cpp:159
     }
-    const int rank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
-    if (rank == 0)
+    if (crank == 0)
         for (int k = tid; k < 12 * N; k += bs) state[k] = x[k];
     if (fl) atomicOr(flags, fl);
     cluster_barrier<CS>();  // no CTA may exit while others still push partials into it
@@ -238,7 +267,7 @@ void fused_preload() {
 }
 
 cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t steps, double t0, double dt, int scheme,
-                                   unsigned* flags, cudaStream_t st) {
+                                   unsigned* flags, cudaStream_t st, unsigned long long* prof) {
     const int cs = fused_cluster_size(p);
     if (cs == 0) return cudaErrorInvalidValue;
     const int64_t n = p.rods * p.m;
@@ -253,6 +282,7 @@ cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t st
     a.chunks = plan.chunks;
     a.lj_on = (p.rods >= 2 && p.lj_well > 0.0) ? 1 : 0;  // propagators.cpp:70
     a.max_disp = 10.0 * p.ds;
+    a.prof = prof;
     int off = 0;
     auto take = [&](int count) {
         const int o = off;

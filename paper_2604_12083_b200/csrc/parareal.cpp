@@ -701,9 +701,13 @@ class HostSlice final : public SliceBackend {
 
 class GpuSlice final : public SliceBackend {
   public:
-    GpuSlice(const pswim_scenario& sc, int device, int64_t fine_steps, int64_t coarse_steps)
+    // space_coarse / space_fine: optional space-group transports (hybrid space x time): the
+    // slice's coarse and fine propagations then shard their MRS over the group, one transport
+    // per context so the two streams' all-gathers never interleave
+    GpuSlice(const pswim_scenario& sc, int device, int64_t fine_steps, int64_t coarse_steps,
+             const pswim_transport* space_coarse = nullptr, const pswim_transport* space_fine = nullptr)
         : device_(device), len_(12 * sc.rod_count * sc.nodes_per_rod), fine_steps_(fine_steps),
-          coarse_steps_(coarse_steps) {
+          coarse_steps_(coarse_steps), sp_c_(space_coarse), sp_f_(space_fine) {
         int lo = 0, hi = 0;
         cudaSetDevice(device);
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -750,11 +754,11 @@ class GpuSlice final : public SliceBackend {
                                                                                                     : fail("download");
     }
     int coarse(int in, double t0, double t1, int out) override {
-        const int rc = cctx_->propagate_async(bufs_[in], t0, t1, PSWIM_EULER, coarse_steps_, 0.0, bufs_[out]);
+        const int rc = cctx_->propagate_async(bufs_[in], t0, t1, PSWIM_EULER, coarse_steps_, 0.0, bufs_[out], sp_c_);
         return rc ? fail(cctx_->err, rc) : PSWIM_OK;
     }
     int fine(int in, double t0, double t1, int out) override {
-        const int rc = fctx_->propagate_async(bufs_[in], t0, t1, PSWIM_RK2, fine_steps_, 0.0, bufs_[out]);
+        const int rc = fctx_->propagate_async(bufs_[in], t0, t1, PSWIM_RK2, fine_steps_, 0.0, bufs_[out], sp_f_);
         return rc ? fail(fctx_->err, rc) : PSWIM_OK;
     }
     int correct(int xp, int gn, int go, int out) override {
@@ -828,6 +832,8 @@ class GpuSlice final : public SliceBackend {
     }
     int device_;
     int64_t len_, fine_steps_, coarse_steps_;
+    const pswim_transport* sp_c_ = nullptr;
+    const pswim_transport* sp_f_ = nullptr;
     pswim_ctx* cctx_ = nullptr;
     pswim_ctx* fctx_ = nullptr;
     cudaStream_t comm_ = nullptr;
@@ -1243,6 +1249,25 @@ int pswim_parareal_rank_gpu(const pswim_plan* plan, const pswim_scenario* sc, in
     try {
         GpuSlice be(*sc, device, fine_steps, coarse_steps);
         return rank_run(*plan, be, *tr, 12 * sc->rod_count * sc->nodes_per_rod, x0, ref_slice, state_out, rep);
+    } catch (const CodeError& e) {
+        return e.code;
+    }
+}
+
+int pswim_parareal_rank_gpu_hybrid(const pswim_plan* plan, const pswim_scenario* sc, int device,
+                                   const pswim_transport* time_tr, const pswim_transport* space_coarse,
+                                   const pswim_transport* space_fine, int64_t fine_steps, int64_t coarse_steps,
+                                   const double* x0, const double* ref_slice, double* state_out, pswim_report* rep) {
+    using namespace pswim;
+    if (plan_check(plan) || !sc || !time_tr || !space_coarse || !space_fine || !x0 || !state_out || !rep ||
+        fine_steps < 1 || coarse_steps < 1)
+        return PSWIM_EINVAL;
+    if (space_coarse->world != space_fine->world || space_coarse->rank != space_fine->rank || !space_coarse->allgather ||
+        !space_fine->allgather)
+        return PSWIM_EINVAL;
+    try {
+        GpuSlice be(*sc, device, fine_steps, coarse_steps, space_coarse, space_fine);
+        return rank_run(*plan, be, *time_tr, 12 * sc->rod_count * sc->nodes_per_rod, x0, ref_slice, state_out, rep);
     } catch (const CodeError& e) {
         return e.code;
     }

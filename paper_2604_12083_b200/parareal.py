@@ -389,9 +389,55 @@ def nccl_transport(device: int):
     return tr
 
 
+def nccl_group_transports(device: int, groups):
+    """One NCCL transport per group this rank belongs to, for a list of disjoint-or-not rank
+    groups (each a list of global torch.distributed ranks).  Every rank walks `groups` in the
+    same order, so communicator creation never deadlocks; the first rank of a group makes
+    its unique id, shared with one all_gather_object.  Returns {group index: transport}."""
+    import torch.distributed as dist
+
+    L = _lib.lib()
+    rank = dist.get_rank()
+    ids = {}
+    for gi, g in enumerate(groups):
+        if g[0] == rank:
+            uid = (C.c_uint8 * 128)()
+            _lib.raise_for(L.pswim_nccl_unique_id(uid), "ncclGetUniqueId failed")
+            ids[gi] = bytes(uid)
+    allids = [None] * dist.get_world_size()
+    dist.all_gather_object(allids, ids)
+    merged = {}
+    for d in allids:
+        merged.update(d)
+    out = {}
+    for gi, g in enumerate(groups):
+        if rank in g:
+            uid = (C.c_uint8 * 128)(*merged[gi])
+            tr = L.pswim_nccl_transport_create(uid, g.index(rank), len(g), int(device))
+            if not tr:
+                raise _lib.PswimError(7, "ncclCommInitRank failed")
+            out[gi] = tr
+    return out
+
+
+def hybrid_groups(world: int, members: int):
+    """Rank layout of hybrid space x time: global rank g = p * members + q is member q of
+    slice p.  Returns (time groups, space groups): time group q = the q-th members of all
+    slices, space group p = the members of slice p (adjacent ranks, NVLink neighbours)."""
+    slices = world // members
+    time_groups = [[p * members + q for p in range(slices)] for q in range(members)]
+    space_groups = [[p * members + q for q in range(members)] for p in range(slices)]
+    return time_groups, space_groups
+
+
 def run_sliced_rank(plan: ParallelPlan, scenario, fine_steps: int, coarse_steps: int, x0, device: int,
-                    transport=None, reference_slice=None) -> RankResult:
-    """This process's slice of a time-sliced pipelined Parareal run on `device` (NCCL)."""
+                    transport=None, reference_slice=None, space=None) -> RankResult:
+    """This process's slice of a time-sliced pipelined Parareal run on `device` (NCCL).
+
+    ``space=(coarse_transport, fine_transport)``: hybrid space x time -- this rank is one
+    member of its slice's space group, and every coarse / fine rhs shards the MRS over that
+    group (pswim_parareal_rank_gpu_hybrid); ``transport`` then connects the same-index members
+    of all slices."""
     _validate(plan)
     L = _lib.lib()
     own = transport is None
@@ -402,10 +448,16 @@ def run_sliced_rank(plan: ParallelPlan, scenario, fine_steps: int, coarse_steps:
     rep, et, ea = _report_arrays(plan.intervals)
     ref = None if reference_slice is None else np.ascontiguousarray(np.asarray(reference_slice, dtype=np.float64))
     try:
-        rc = L.pswim_parareal_rank_gpu(C.byref(plan.to_c()), C.byref(sc), int(device), tr, int(fine_steps),
-                                       int(coarse_steps), x0.ctypes.data_as(C.POINTER(C.c_double)),
-                                       ref.ctypes.data_as(C.POINTER(C.c_double)) if ref is not None else None,
-                                       out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep))
+        refp = ref.ctypes.data_as(C.POINTER(C.c_double)) if ref is not None else None
+        if space is None:
+            rc = L.pswim_parareal_rank_gpu(C.byref(plan.to_c()), C.byref(sc), int(device), tr, int(fine_steps),
+                                           int(coarse_steps), x0.ctypes.data_as(C.POINTER(C.c_double)), refp,
+                                           out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep))
+        else:
+            rc = L.pswim_parareal_rank_gpu_hybrid(C.byref(plan.to_c()), C.byref(sc), int(device), tr, space[0],
+                                                  space[1], int(fine_steps), int(coarse_steps),
+                                                  x0.ctypes.data_as(C.POINTER(C.c_double)), refp,
+                                                  out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep))
     finally:
         if own:
             L.pswim_nccl_transport_destroy(tr)

@@ -89,3 +89,19 @@ def test_rank_driver_tolerance_stop():
         assert et == res.report.eta_tilde
         assert conv == res.report.converged
         assert np.array_equal(np.array(state), res.states[rank + 1])
+
+
+def test_hybrid_rank_layout():
+    """Hybrid space x time layout (bench N >= 4): member q of slice p is global rank
+    p * members + q; time groups join same-index members, space groups are adjacent ranks."""
+    from paper_2604_12083_b200.parareal import hybrid_groups
+
+    tg, sg = hybrid_groups(8, 2)
+    assert tg == [[0, 2, 4, 6], [1, 3, 5, 7]]
+    assert sg == [[0, 1], [2, 3], [4, 5], [6, 7]]
+    tg, sg = hybrid_groups(8, 4)
+    assert tg == [[0, 4], [1, 5], [2, 6], [3, 7]] and sg == [[0, 1, 2, 3], [4, 5, 6, 7]]
+    for world, members in ((4, 2), (8, 2), (8, 4)):
+        tg, sg = hybrid_groups(world, members)
+        assert sorted(r for g in tg for r in g) == list(range(world))
+        assert sorted(r for g in sg for r in g) == list(range(world))
