@@ -336,9 +336,8 @@ pswim_ctx* pswim_create(int device, const pswim_scenario* sc, int stream_priorit
             return nullptr;
         }
         if (ctx->rp.rods >= 2 && ctx->rp.lj_well > 0.0 && ctx->rs.total_nodes >= kLjCellsMinNodes) {
-            // cell-list workspace + one warm-up pass (loads its sort kernels, see preload_kernels)
-            if (cudaMemsetAsync(ctx->d_mid, 0, sizeof(double) * 4 * n3, ctx->stream) != cudaSuccess ||
-                lj_cells_launch(ctx->rp, ctx->d_mid, ctx->d_lj, &ctx->lj_work, ctx->stream) != cudaSuccess) {
+            // cell-list workspace + one sort (loads the sort kernels, see preload_kernels)
+            if (lj_cells_reserve(ctx->rs.total_nodes, &ctx->lj_work, ctx->stream) != cudaSuccess) {
                 delete ctx;
                 return nullptr;
             }

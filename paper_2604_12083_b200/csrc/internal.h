@@ -100,6 +100,7 @@ struct LjWork {
 };
 int lj_buckets(int64_t n);
 cudaError_t lj_cells_launch(const RodParams& p, const double* state, double* forces, LjWork* w, cudaStream_t st);
+cudaError_t lj_cells_reserve(int64_t total, LjWork* w, cudaStream_t st);
 void lj_cells_preload();
 // all-pairs kernel below this many nodes in LJ auto mode, cell list above
 constexpr int64_t kLjCellsMinNodes = 2048;

@@ -56,6 +56,15 @@ __global__ void lj_bounds_kernel(const double* __restrict__ state, int n, int m,
     pos[3 * p + 2] = x[2];
 }
 
+__device__ __forceinline__ int lower_bound_idx(const int* __restrict__ idx, int lo, int hi, int v) {
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (idx[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
 __global__ void __launch_bounds__(256)
 lj_cells_kernel(const double* __restrict__ pos, const int* __restrict__ idx, const int2* __restrict__ rk,
                 const int* __restrict__ start, const int* __restrict__ end, int n, double inv_h, unsigned mask, LjArgs a,
@@ -66,6 +75,7 @@ lj_cells_kernel(const double* __restrict__ pos, const int* __restrict__ idx, con
     const int2 me = rk[p];
     const double xi = pos[3 * p], yi = pos[3 * p + 1], zi = pos[3 * p + 2];
     const int cx = cell_coord(xi, inv_h), cy = cell_coord(yi, inv_h), cz = cell_coord(zi, inv_h);
+    const int wlo = max(me.x * a.m, i - (a.excl - 1)), whi = min(me.x * a.m + a.m - 1, i + (a.excl - 1));
     unsigned seen[27];
     double fx = 0.0, fy = 0.0, fz = 0.0;
 #pragma unroll
@@ -76,8 +86,13 @@ lj_cells_kernel(const double* __restrict__ pos, const int* __restrict__ idx, con
 #pragma unroll
         for (int e = 0; e < c; ++e) dup |= seen[e] == b;
         if (dup) continue;
-        const int q1 = end[b];
-        for (int q = start[b]; q < q1; ++q) {
+        const int q0 = start[b], q1 = end[b];
+        // members are in ascending node order: the same-rod window |k_i - k_j| < excl, which
+        // the pair law skips, is one contiguous run [qa, qb) found by binary search
+        const int qa = lower_bound_idx(idx, q0, q1, wlo), qb = lower_bound_idx(idx, qa, q1, whi + 1);
+        for (int q = q0; q < q1; ++q) {
+            if (q == qa) q = qb;
+            if (q >= q1) break;
             const int2 o = rk[q];
             lj_pair(a, me.x, me.y, o.x, o.y, xi - pos[3 * q], yi - pos[3 * q + 1], zi - pos[3 * q + 2], fx, fy, fz);
         }
@@ -102,13 +117,9 @@ int lj_buckets(int64_t n) {
     return (int)h;
 }
 
-cudaError_t lj_cells_launch(const RodParams& p, const double* state, double* forces, LjWork* w, cudaStream_t st) {
-    const int64_t total = p.rods * p.m;
-    if (total == 0) return cudaSuccess;
+namespace {
+cudaError_t lj_grow(int64_t total, int H, int bits, LjWork* w, cudaStream_t st) {
     const int n = (int)total;
-    const int H = lj_buckets(total);
-    int bits = 0;
-    while ((1 << bits) < H) ++bits;
     cudaError_t e;
     if (w->cap_nodes < total || w->cap_buckets < H) {
         w->release();
@@ -130,6 +141,19 @@ cudaError_t lj_cells_launch(const RodParams& p, const double* state, double* for
         w->cap_nodes = total;
         w->cap_buckets = H;
     }
+    return cudaSuccess;
+}
+}  // namespace
+
+cudaError_t lj_cells_launch(const RodParams& p, const double* state, double* forces, LjWork* w, cudaStream_t st) {
+    const int64_t total = p.rods * p.m;
+    if (total == 0) return cudaSuccess;
+    const int n = (int)total;
+    const int H = lj_buckets(total);
+    int bits = 0;
+    while ((1 << bits) < H) ++bits;
+    cudaError_t e = lj_grow(total, H, bits, w, st);
+    if (e != cudaSuccess) return e;
     const double inv_h = 1.0 / p.lj_cutoff;
     const unsigned mask = (unsigned)H - 1u;
     const unsigned blocks = (unsigned)((n + 255) / 256);
@@ -145,6 +169,21 @@ cudaError_t lj_cells_launch(const RodParams& p, const double* state, double* for
     lj_cells_kernel<<<blocks, 256, 0, st>>>(w->pos, w->idx_sorted, w->rk, w->cell_start, w->cell_end, n, inv_h, mask,
                                            lj_args(p), forces);
     return cudaGetLastError();
+}
+
+cudaError_t lj_cells_reserve(int64_t total, LjWork* w, cudaStream_t st) {
+    // workspace for `total` nodes + one sort on it: loads the radix-sort kernels this size
+    // selects (CUDA lazy loading, see preload_kernels) without a pair pass
+    const int n = (int)total;
+    const int H = lj_buckets(total);
+    int bits = 0;
+    while ((1 << bits) < H) ++bits;
+    cudaError_t e = lj_grow(total, H, bits, w, st);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(w->key, 0, sizeof(unsigned) * n, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(w->idx, 0, sizeof(int) * n, st)) != cudaSuccess) return e;
+    size_t tmp = w->tmp_bytes;
+    return cub::DeviceRadixSort::SortPairs(w->tmp, tmp, w->key, w->key_sorted, w->idx, w->idx_sorted, n, 0, bits, st);
 }
 
 void lj_cells_preload() {
