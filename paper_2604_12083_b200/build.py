@@ -22,7 +22,11 @@ LIB = os.path.join(HERE, "libpswim.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 HOST_CXX = "/usr/bin/g++"
-COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-ccbin", HOST_CXX,
+# -fmad=false: no automatic FMA contraction.  Contraction decisions depend on the inlining
+# context (e.g. whether a product has other uses), so the same device routine inlined into
+# two kernels could round differently; the fused small-system kernel and the launched
+# kernels must agree bitwise.  Every FMA on the path is an explicit fma() call instead.
+COMMON = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC", "-ccbin", HOST_CXX,
           "-I" + os.path.join(ROOT, "include")]
 
 
@@ -48,6 +52,15 @@ def _compile(src: str) -> tuple[str, str]:
 
 def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    # objects are rebuilt when the compile flags change, not only when sources do
+    stamp = os.path.join(BUILD, "flags.txt")
+    flags = " ".join([NVCC, *ARCH, *COMMON])
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        for f in os.listdir(BUILD):
+            if f.endswith(".o"):
+                os.remove(os.path.join(BUILD, f))
+        with open(stamp, "w") as fh:
+            fh.write(flags)
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         results = list(ex.map(_compile, srcs))

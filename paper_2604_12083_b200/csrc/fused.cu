@@ -15,6 +15,9 @@
 // same N, so a fused propagate is bitwise identical to the multi-kernel one.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace cg = cooperative_groups;
@@ -142,25 +145,20 @@ __device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, doub
     }
     __syncthreads();
     pc.mark(3);
-    for (int il = tid; il < nloc; il += bs) {
-        double sum[6];
-#pragma unroll
-        for (int q = 0; q < 6; ++q) sum[q] = lpart[il * 6 + q];
-        for (int c = 1; c < a.chunks; ++c)
-#pragma unroll
-            for (int q = 0; q < 6; ++q) sum[q] += lpart[(c * tpc + il) * 6 + q];
+    // one thread per (target, component): the chunk partials summed in chunk order 0..C-1
+    // (mrs.cu's last-CTA reduction, bitwise), then pushed to every CTA of the cluster
+    for (int w = tid; w < nloc * 6; w += bs) {
+        const int il = w / 6, q = w - 6 * il;
+        double sum = lpart[w];
+#pragma unroll 4
+        for (int c = 1; c < a.chunks; ++c) sum += lpart[(c * tpc + il) * 6 + q];
         const int i = i0 + il;
         if constexpr (CS > 1) {
             cg::cluster_group cl = cg::this_cluster();
-#pragma unroll 1
-            for (int rr = 0; rr < CS; ++rr) {
-                double* dst = cl.map_shared_rank(vel, rr) + 6 * i;
 #pragma unroll
-                for (int q = 0; q < 6; ++q) dst[q] = sum[q];
-            }
+            for (int rr = 0; rr < CS; ++rr) cl.map_shared_rank(vel, rr)[6 * i + q] = sum;
         } else {
-#pragma unroll
-            for (int q = 0; q < 6; ++q) vel[6 * i + q] = sum[q];
+            vel[6 * i + q] = sum;
         }
     }
     if (a.prof) __syncthreads();  // phase timer only: end of the push as one CTA-wide instant
@@ -224,6 +222,10 @@ cudaError_t launch_cs(const FusedArgs& a, size_t smem, double* state, int64_t st
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(fused_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
+        if (CS > 8) {
+            e = cudaFuncSetAttribute(fused_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+        }
         configured = true;
     }
     cudaLaunchConfig_t cfg{};
@@ -248,8 +250,17 @@ int fused_cluster_size(const RodParams& p) {
     const int64_t n = p.rods * p.m;
     if (n > 256 || n < 2) return 0;
     const MrsPlan plan = mrs_plan(n, n);
+    static const int max_cs = [] {
+        const char* e = std::getenv("PSWIM_FUSED_MAX_CLUSTER");
+        const int v = e ? std::atoi(e) : 8;
+        return (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) ? v : 8;
+    }();
+    static const int min_tpc = [] {
+        const char* e = std::getenv("PSWIM_FUSED_MIN_TARGETS");
+        return e ? std::max(1, std::atoi(e)) : 12;
+    }();
     int cs = 1;
-    while (cs < 8 && (n + 2 * cs - 1) / (2 * cs) >= 12) cs *= 2;  // >= 12 targets per CTA
+    while (cs < max_cs && (n + 2 * cs - 1) / (2 * cs) >= min_tpc) cs *= 2;  // >= min_tpc targets per CTA
     const int64_t tpc = (n + cs - 1) / cs;
     // shared memory: x, xm (12n each), pos/f/n/lj (3n each), seg, rec (18n), local partials
     // (chunks x tpc x 6), velocities (2 x 6n)
@@ -264,6 +275,7 @@ void fused_preload() {
     cudaFuncGetAttributes(&a, fused_kernel<2>);
     cudaFuncGetAttributes(&a, fused_kernel<4>);
     cudaFuncGetAttributes(&a, fused_kernel<8>);
+    cudaFuncGetAttributes(&a, fused_kernel<16>);
 }
 
 cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t steps, double t0, double dt, int scheme,
@@ -306,7 +318,8 @@ cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t st
         case 1: return launch_cs<1>(a, smem, state, steps, t0, dt, scheme, flags, st);
         case 2: return launch_cs<2>(a, smem, state, steps, t0, dt, scheme, flags, st);
         case 4: return launch_cs<4>(a, smem, state, steps, t0, dt, scheme, flags, st);
-        default: return launch_cs<8>(a, smem, state, steps, t0, dt, scheme, flags, st);
+        case 8: return launch_cs<8>(a, smem, state, steps, t0, dt, scheme, flags, st);
+        default: return launch_cs<16>(a, smem, state, steps, t0, dt, scheme, flags, st);
     }
 }
 
