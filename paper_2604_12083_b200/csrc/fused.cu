@@ -19,6 +19,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -26,6 +27,7 @@ namespace pswim {
 namespace {
 
 constexpr int kFusedThreads = 512;
+constexpr int kFrontNodes = 30;  // nodes owned per warp in the warp-tiled front pass
 
 struct FusedArgs {
     RodArgs rod;
@@ -38,6 +40,8 @@ struct FusedArgs {
     double max_disp;
     // shared-memory offsets (doubles)
     int off_x, off_xm, off_pos, off_f, off_n, off_seg, off_lj, off_rec, off_part, off_vel;
+    int off_x2, off_tile;  // second step-start state buffer; per-warp front tiles (32 x 12)
+    int off_bar;           // two mbarriers (velocity buffers)
     int part_stride;  // unused (kept for layout clarity)
     unsigned long long* prof;  // kFusedPhases clock64 counters (CTA 0, thread 0), nullptr = off
 };
@@ -67,49 +71,100 @@ __device__ __forceinline__ void cluster_barrier() {
     }
 }
 
-// rhs (propagators.cpp:38-91) of the state `xs` at time t into vel[6 n] = (u, w) per node.
+// Front half of an rhs (propagators.cpp:38-91): produce the rhs state -- `src` itself
+// (vadv == nullptr) or dst = advance_state(src, vadv, h) node by node (propagators.cpp:93-124)
+// -- and, on that state, the segment and nodal loads and the MRS source records (rec) and
+// target positions (pos).  Returns the rhs state.
+//
+// Systems without LJ take a warp-tiled pass with no CTA barrier inside: warp w covers nodes
+// 30 w - 1 + lane (lanes 1..30 own a node, lanes 0 and 31 recompute a neighbour's advance),
+// advances them into a per-warp tile, computes segment (g, g+1) per lane and gets segment
+// g - 1 by one shuffle -- the layout of rod_loads_wtma_kernel.  LJ needs every advanced
+// position first, so LJ systems take the phased version.
 template <int CS>
-__device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, double t, double* vel, unsigned& fl,
-                          PhaseClock& pc) {
+__device__ const double* fused_front(const FusedArgs& a, double* sm, const double* src, const double* vadv, double h,
+                                     double* dst, double t, unsigned& fl, PhaseClock& pc) {
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n, m = a.m, nseg = a.rods * (m - 1);
     double* pos = sm + a.off_pos;
+    double2* rec = reinterpret_cast<double2*>(sm + a.off_rec);
+    if (!a.lj_on) {
+        const int warp = tid >> 5, lane = tid & 31, nw = (N + kFrontNodes - 1) / kFrontNodes;
+        if (warp < nw) {
+            const int base = kFrontNodes * warp - 1, g = base + lane;
+            const bool valid = g >= 0 && g < N;
+            double* tile = sm + a.off_tile + warp * 32 * 12;  // slot l = node base + l
+            // origin of the MRS coordinates: node 0 of the rhs state (advance_node's position
+            // update, same operations)
+            const d3 o = vadv ? ld3(src) + ld3(vadv) * h : ld3(src);
+            if (valid && vadv) fl |= advance_node(src + 12 * g, vadv + 6 * g, vadv + 6 * g + 3, h, a.max_disp, tile + 12 * lane);
+            __syncwarp();
+            pc.mark(1);
+            const int rod = valid ? g / m : 0, k = valid ? g - rod * m : 0;
+            const double* xs = vadv ? tile + 12 * (rod * m - base) : src + 12 * rod * m;  // rod's node 0
+            double seg[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            if (valid && lane < 31 && k + 1 < m)
+                if (!rod_segment(a.rod, xs, k, t, seg)) fl |= kFlagDegenerate;
+            double prev[6];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) prev[q] = __shfl_up_sync(0xffffffffu, seg[q], 1);
+            pc.mark(2);
+            if (valid && lane >= 1 && lane <= kFrontNodes) {
+                const d3 xk = ld3(xs + 12 * k);
+                const d3 xnext = k + 1 < m ? ld3(xs + 12 * (k + 1)) : xk;
+                const d3 xprev = k > 0 ? ld3(xs + 12 * (k - 1)) : xk;
+                if (vadv)
+#pragma unroll
+                    for (int q = 0; q < 12; ++q) dst[12 * g + q] = xs[12 * k + q];
+                d3 f, tq;
+                node_loads(a.rod, k, seg, prev, xprev, xk, xnext, f, tq);
+                st3(pos + 3 * g, xk);
+                double2 r[9];
+                if (!mrs_stage(&xk.x, 3, &f.x, &tq.x, 0, o.x, o.y, o.z, a.mc.scale, r)) fl |= kFlagNonFinite;
+#pragma unroll
+                for (int q = 0; q < 9; ++q) rec[q * N + g] = r[q];
+            }
+        }
+        __syncthreads();
+        pc.mark(0);
+        return vadv ? dst : src;
+    }
+    // phased (LJ) version
+    if (vadv) {
+        for (int i = tid; i < N; i += bs)
+            fl |= advance_node(src + 12 * i, vadv + 6 * i, vadv + 6 * i + 3, h, a.max_disp, dst + 12 * i);
+        __syncthreads();
+    }
+    const double* xs = vadv ? dst : src;
     double* fo = sm + a.off_f;
     double* no = sm + a.off_n;
     double* seg = sm + a.off_seg;
     double* ljf = sm + a.off_lj;
-    double2* rec = reinterpret_cast<double2*>(sm + a.off_rec);
-
     for (int s = tid; s < nseg; s += bs) {
         const int r = s / (m - 1), k = s % (m - 1);
         if (!rod_segment(a.rod, xs + 12 * m * r, k, t, seg + 6 * s)) fl |= kFlagDegenerate;
     }
-    if (a.lj_on) {
-        for (int i = tid; i < N; i += bs) {
-            double fx = 0, fy = 0, fz = 0;
-            const double xi = xs[12 * i], yi = xs[12 * i + 1], zi = xs[12 * i + 2];
-            const int ri = i / m, ki = i - ri * m;
-            for (int rj = 0, j = 0; rj < a.lj.rods; ++rj)
-                for (int kj = 0; kj < m; ++kj, ++j)
-                    lj_pair(a.lj, ri, ki, rj, kj, xi - xs[12 * j], yi - xs[12 * j + 1], zi - xs[12 * j + 2], fx, fy,
-                            fz);
-            ljf[3 * i] = fx;
-            ljf[3 * i + 1] = fy;
-            ljf[3 * i + 2] = fz;
-        }
+    for (int i = tid; i < N; i += bs) {
+        double fx = 0, fy = 0, fz = 0;
+        const double xi = xs[12 * i], yi = xs[12 * i + 1], zi = xs[12 * i + 2];
+        const int ri = i / m, ki = i - ri * m;
+        for (int rj = 0, j = 0; rj < a.lj.rods; ++rj)
+            for (int kj = 0; kj < m; ++kj, ++j)
+                lj_pair(a.lj, ri, ki, rj, kj, xi - xs[12 * j], yi - xs[12 * j + 1], zi - xs[12 * j + 2], fx, fy, fz);
+        ljf[3 * i] = fx;
+        ljf[3 * i + 1] = fy;
+        ljf[3 * i + 2] = fz;
     }
     __syncthreads();
-    pc.mark(0);
     for (int g = tid; g < N; g += bs) {
         const int r = g / m, k = g % m;
         d3 f, tq;
         rod_node(a.rod, xs + 12 * m * r, seg + 6 * (m - 1) * r, k, f, tq);
-        if (a.lj_on) f = f + ld3(ljf + 3 * g) * a.rod.inv_ds;
+        f = f + ld3(ljf + 3 * g) * a.rod.inv_ds;
         st3(pos + 3 * g, ld3(xs + 12 * g));
         st3(fo + 3 * g, f);
         st3(no + 3 * g, tq);
     }
     __syncthreads();
-    pc.mark(1);
     // stage every source relative to node 0 (the single target block's origin in mrs.cu)
     const double ox = pos[0], oy = pos[1], oz = pos[2];
     for (int j = tid; j < N; j += bs) {
@@ -119,7 +174,45 @@ __device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, doub
         for (int q = 0; q < 9; ++q) rec[q * N + j] = r[q];
     }
     __syncthreads();
-    pc.mark(2);
+    pc.mark(0);
+    return xs;
+}
+
+// Back half of an rhs: the O(N^2) MRS of the staged sources into vel[6 n] = (u, w) per node.
+__device__ __forceinline__ uint32_t cluster_addr(uint32_t local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+
+// Asynchronous remote store of one double into CTA `rank`'s shared memory whose completion
+// is counted (8 bytes of transaction) on that CTA's mbarrier.
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr), "d"(v),
+                 "r"(rbar)
+                 : "memory");
+}
+
+// Wait until this CTA's velocity buffer of the given mbarrier holds all N x 6 values of the
+// rhs (every CTA's st.async pushes counted as transaction bytes): thread 0 posts the
+// expected bytes and the one arrival, every thread waits on the phase parity.
+template <int CS>
+__device__ __forceinline__ void vel_wait(uint64_t* vbar, uint32_t& phase, int n) {
+    if constexpr (CS > 1) {
+        if (threadIdx.x == 0) mbar_expect_tx(vbar, (uint32_t)(6 * n * sizeof(double)));
+        mbar_wait(vbar, phase & 1u);
+        ++phase;
+    } else {
+        __syncthreads();
+    }
+}
+
+template <int CS>
+__device__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t* vbar, PhaseClock& pc) {
+    const int tid = threadIdx.x, bs = blockDim.x, N = a.n;
+    const double* pos = sm + a.off_pos;
+    const double2* rec = reinterpret_cast<const double2*>(sm + a.off_rec);
+    const double ox = pos[0], oy = pos[1], oz = pos[2];
     // MRS: this CTA owns targets [i0, i1); items (target, source chunk) computed here, the
     // chunk partials reduced locally in fixed order (mrs.cu's last-CTA reduction), and each
     // target's 6 velocities pushed to every CTA of the cluster through DSMEM.
@@ -154,17 +247,17 @@ __device__ void fused_rhs(const FusedArgs& a, double* sm, const double* xs, doub
         for (int c = 1; c < a.chunks; ++c) sum += lpart[(c * tpc + il) * 6 + q];
         const int i = i0 + il;
         if constexpr (CS > 1) {
-            cg::cluster_group cl = cg::this_cluster();
+            // st.async into every CTA (itself included), completion counted on its mbarrier:
+            // no cluster barrier and no GPU-scope fence per rhs
+            const uint32_t laddr = smem_u32(vel + 6 * i + q), lbar = smem_u32(vbar);
 #pragma unroll
-            for (int rr = 0; rr < CS; ++rr) cl.map_shared_rank(vel, rr)[6 * i + q] = sum;
+            for (int rr = 0; rr < CS; ++rr) st_async_f64(cluster_addr(laddr, rr), sum, cluster_addr(lbar, rr));
         } else {
             vel[6 * i + q] = sum;
         }
     }
     if (a.prof) __syncthreads();  // phase timer only: end of the push as one CTA-wide instant
     pc.mark(4);
-    cluster_barrier<CS>();
-    pc.mark(5);
 }
 
 template <int CS>
@@ -176,41 +269,68 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
     double* x = sm + a.off_x;
     double* xm = sm + a.off_xm;
     for (int k = tid; k < 12 * N; k += bs) x[k] = state[k];
-    __syncthreads();
+    uint64_t* vbar = reinterpret_cast<uint64_t*>(sm + a.off_bar);  // one mbarrier per velocity buffer
+    if (tid == 0) {
+        mbar_init(&vbar[0], 1);
+        mbar_init(&vbar[1], 1);
+        fence_mbar_init();
+    }
+    uint32_t vphase[2] = {0u, 0u};
+    cluster_barrier<CS>();  // barriers initialised before any CTA pushes into them
     unsigned fl = 0;
     int parity = 0;
     double t = t0;
     const int crank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
     PhaseClock pc{(a.prof && tid == 0 && crank == 0) ? a.prof : nullptr, clock64()};
     // velocities are double-buffered: a CTA that runs ahead pushes the next rhs into the
-    // other buffer while slower CTAs still read this one (the next cluster barrier orders it)
+    // other buffer while slower CTAs still read this one (the next cluster barrier orders it).
+    // The advance that produces an rhs state runs inside that rhs's front pass (src -> dst,
+    // never in place: overlap lanes read neighbours' old states), so the step-start state
+    // alternates between x and x2; xm holds the RK2 midpoint.
+    double* xb[2] = {x, sm + a.off_x2};
+    int cur = 0;
+    const double* vadv = nullptr;  // velocities of the pending advance (none before step 0)
+    double h = 0.0;
+    int vp = 0;  // velocity buffer holding vadv
     for (int64_t s = 0; s < steps; ++s) {
         double* vel = sm + a.off_vel + parity * 6 * N;
-        fused_rhs<CS>(a, sm, x, t, vel, fl, pc);
+        if (vadv) vel_wait<CS>(&vbar[vp], vphase[vp], N);
+        pc.mark(5);
+        fused_front<CS>(a, sm, vadv ? xb[cur ^ 1] : xb[cur], vadv, h, xb[cur], t, fl, pc);
+        fused_mrs<CS>(a, sm, vel, &vbar[parity], pc);
+        const int p1 = parity;
         parity ^= 1;
         if (scheme == PSWIM_EULER) {
-            for (int i = tid; i < N; i += bs)
-                fl |= advance_node(x + 12 * i, vel + 6 * i, vel + 6 * i + 3, dt, a.max_disp, x + 12 * i);
-            __syncthreads();
-            pc.mark(6);
+            vadv = vel;
+            vp = p1;
+            h = dt;
         } else {
-            // step_rk2, propagators.cpp:130-133
-            for (int i = tid; i < N; i += bs)
-                fl |= advance_node(x + 12 * i, vel + 6 * i, vel + 6 * i + 3, 0.5 * dt, a.max_disp, xm + 12 * i);
-            __syncthreads();
-            pc.mark(6);
-            vel = sm + a.off_vel + parity * 6 * N;
-            fused_rhs<CS>(a, sm, xm, t + 0.5 * dt, vel, fl, pc);
+            // step_rk2, propagators.cpp:130-133: mid = advance(x, v1, dt/2), out = advance(x, v2, dt)
+            double* vel2 = sm + a.off_vel + parity * 6 * N;
+            vel_wait<CS>(&vbar[p1], vphase[p1], N);
+            pc.mark(5);
+            fused_front<CS>(a, sm, xb[cur], vel, 0.5 * dt, xm, t + 0.5 * dt, fl, pc);
+            fused_mrs<CS>(a, sm, vel2, &vbar[parity], pc);
+            vp = parity;
             parity ^= 1;
-            for (int i = tid; i < N; i += bs)
-                fl |= advance_node(x + 12 * i, vel + 6 * i, vel + 6 * i + 3, dt, a.max_disp, x + 12 * i);
-            __syncthreads();
-            pc.mark(6);
+            vadv = vel2;
+            h = dt;
         }
-        t += dt;  // propagators.cpp:159
+        cur ^= 1;  // the next state goes to the other buffer
+        t += dt;   // propagators.cpp:159
+    }
+    // the last step's closing advance (no rhs follows)
+    double* out = xb[cur];
+    if (vadv) {
+        vel_wait<CS>(&vbar[vp], vphase[vp], N);
+        pc.mark(5);
+        for (int i = tid; i < N; i += bs)
+            fl |= advance_node(xb[cur ^ 1] + 12 * i, vadv + 6 * i, vadv + 6 * i + 3, h, a.max_disp, out + 12 * i);
+        __syncthreads();
+        pc.mark(6);
     }
     if (crank == 0)
-        for (int k = tid; k < 12 * N; k += bs) state[k] = x[k];
+        for (int k = tid; k < 12 * N; k += bs) state[k] = out[k];
     if (fl) atomicOr(flags, fl);
     cluster_barrier<CS>();  // no CTA may exit while others still push partials into it
 }
@@ -263,8 +383,9 @@ int fused_cluster_size(const RodParams& p) {
     while (cs < max_cs && (n + 2 * cs - 1) / (2 * cs) >= min_tpc) cs *= 2;  // >= min_tpc targets per CTA
     const int64_t tpc = (n + cs - 1) / cs;
     // shared memory: x, xm (12n each), pos/f/n/lj (3n each), seg, rec (18n), local partials
-    // (chunks x tpc x 6), velocities (2 x 6n)
-    const int64_t doubles = 24 * n + 12 * n + 6 * p.rods * (p.m - 1) + 18 * n + plan.chunks * tpc * 6 + 12 * n + 16;
+    // (chunks x tpc x 6), velocities (2 x 6n), x2 (12n), front tiles (warps x 32 x 12)
+    const int64_t doubles = 24 * n + 12 * n + 6 * p.rods * (p.m - 1) + 18 * n + plan.chunks * tpc * 6 + 12 * n + 16 +
+                            12 * n + ((n + kFrontNodes - 1) / kFrontNodes) * 32 * 12 + 2;
     if (doubles * 8 > 220 * 1024) return 0;
     return cs;
 }
@@ -313,6 +434,9 @@ cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t st
     a.part_stride = 0;
     a.off_part = take(plan.chunks * tpc * 6);
     a.off_vel = take(12 * a.n);
+    a.off_x2 = take(12 * a.n);
+    a.off_tile = take(((a.n + kFrontNodes - 1) / kFrontNodes) * 32 * 12);
+    a.off_bar = take(2);
     const size_t smem = (size_t)off * sizeof(double);
     switch (cs) {
         case 1: return launch_cs<1>(a, smem, state, steps, t0, dt, scheme, flags, st);

@@ -268,16 +268,8 @@ rod_loads_wtma_kernel(RodArgs p, int total, const double* __restrict__ state, do
             if (wn < ntiles) issue(wn, s);
         }
         if (lane != 0 && valid) {
-            // nodal_loads (rod.cpp:93-106), the operation order of rod_node
-            const d3 zero = mk3(0, 0, 0);
-            const d3 f_plus = k < m - 1 ? mk3(seg[0], seg[1], seg[2]) : zero;
-            const d3 f_minus = k > 0 ? mk3(prev[0], prev[1], prev[2]) : zero;
-            const d3 n_plus = k < m - 1 ? mk3(seg[3], seg[4], seg[5]) : zero;
-            const d3 n_minus = k > 0 ? mk3(prev[3], prev[4], prev[5]) : zero;
-            d3 f = (f_plus - f_minus) * p.inv_ds;
-            d3 tq = (n_plus - n_minus) * p.inv_ds;
-            if (k < m - 1) tq = tq + cross((xnext - xk) * p.inv_ds, f_plus) * 0.5;
-            if (k > 0) tq = tq + cross((xk - xprev) * p.inv_ds, f_minus) * 0.5;
+            d3 f, tq;
+            node_loads(p, k, seg, prev, xprev, xk, xnext, f, tq);  // nodal_loads, rod.cpp:93-106
             const int64_t g3 = 3 * (int64_t)g;
             if (lj) f = f + ld3(lj + g3) * p.inv_ds;  // propagators.cpp:70-74
             if (extra_f) {                           // propagators.cpp:75-84

@@ -10,7 +10,7 @@ import torch
 from paper_2604_12083_b200.device import Context, dptr
 from paper_2604_12083_b200.scenario import ScenarioConfig, build_initial_state, make_scenario
 
-PHASES = ["segments+lj", "nodes", "stage", "mrs_pairs", "reduce+push", "cluster_barrier", "advance"]
+PHASES = ["front: nodes+stage (+phased)", "front: advance", "front: segments", "mrs_pairs", "reduce+push", "velocity wait", "final advance"]
 
 
 def profile(kw, steps=2000):
@@ -33,7 +33,7 @@ def profile(kw, steps=2000):
     print(f"{kw}: cluster {cs}, {us_step:.2f} us/RK2 step ({1e6 / us_step:.0f} steps/s incl. timer), "
           f"{tot / steps:.0f} cycles/step")
     for name, c in zip(PHASES, cyc):
-        print(f"   {name:16s} {c / steps:8.0f} cycles/step  {100 * c / tot:5.1f} %")
+        print(f"   {name:28s} {c / steps:8.0f} cycles/step  {100 * c / tot:5.1f} %")
     ctx.close()
 
 
