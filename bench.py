@@ -296,9 +296,11 @@ def run_ours(args) -> None:
         sys.path.insert(0, os.path.join(ROOT, "tools"))
         from probe_rod import hbm_kernels
 
-        hbm = hbm_kernels(local)
+        with ClockSampler(local) as hclk:
+            hbm = hbm_kernels(local)
         for v in hbm.values():
             v["frac_of_measured_hbm"] = v["GB_per_s"] / _hbm_peak()
+        hbm["clocks"] = hclk.summary()
         try:
             from probe_lj import lj_times
 
@@ -583,7 +585,9 @@ def parareal_1gpu_leg(sc, x0, local, n=8, fine=1000, coarse=100):
     for l in (1, 2):
         plan.max_iterations = l
         pr.run_gpu(plan, sc, fine, coarse, x0, device=local)  # warm-up
-        res = pr.run_gpu(plan, sc, fine, coarse, x0, reference=serial.states, device=local)
+        with ClockSampler(local) as pclk:
+            res = pr.run_gpu(plan, sc, fine, coarse, x0, reference=serial.states, device=local)
+        out[f"clocks_l{l}"] = pclk.summary()
         out[f"l{l}"] = {"value": n * fine / res.report.wall_seconds, "unit": "steps/s",
                         "speedup_vs_serial_fine": serial_wall / res.report.wall_seconds, "eta": res.report.eta[-1]}
     return {"workload": f"pipelined Parareal on one B200, flagellum 1x100, n={n} intervals x {fine} RK2 "

@@ -210,3 +210,28 @@ def test_simulate_driver(gpu, oracle, tmp_path):
     for key in ("initialization", "velocity_computation", "triad_update"):
         assert key in d["timings"]
     assert d["timings"]["velocity_computation"] > 0
+
+
+def test_fused_phase_profile(gpu):
+    """pswim_fused_profile: the fused propagate with its in-kernel phase timer on returns the
+    same state as the plain fused propagate and non-zero cycles for the phases it runs."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2604_12083_b200.device import Context, dptr
+    from paper_2604_12083_b200.propagators import StepperConfig, propagate
+    from paper_2604_12083_b200.scenario import build_initial_state
+
+    sc = scen(rod_count=1, nodes_per_rod=100)
+    x = build_initial_state(sc)
+    ctx = Context(0, sc)
+    assert ctx.lib.pswim_set_fused(ctx.handle, 1) >= 1
+    want = propagate(x, 0.0, 2e-4, StepperConfig(0.0, 1, 20), sc, ctx=ctx)
+    dx = torch.as_tensor(x, device=gpu)
+    out = torch.empty_like(dx)
+    cyc = (C.c_uint64 * 7)()
+    ctx.check(ctx.lib.pswim_fused_profile(ctx.handle, dptr(dx), 0.0, 2e-4, 1, 20, dptr(out), cyc))
+    assert np.array_equal(out.cpu().numpy(), want)
+    assert all(cyc[i] > 0 for i in (0, 1, 2, 3, 4, 5, 6))
+    ctx.close()
