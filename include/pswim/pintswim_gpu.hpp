@@ -119,6 +119,19 @@ inline pintswim::Rot3 sqrt_rotation(const pintswim::Rot3& r, int device = 0) {
     return s;
 }
 
+// pintswim::lj_repulsion (rod.cpp:124-174) on the device for the rods of scenario `sc` (the
+// reference call site propagators.cpp:71 passes sc.lj and sc.lj_self_exclusion, which the
+// context derives from the same ScenarioConfig): all-pairs below 2048 nodes, cell list above.
+inline std::vector<pintswim::Vec3> lj_repulsion(const std::vector<pintswim::RodState>& rods,
+                                                const pintswim::Scenario& sc, int device = 0) {
+    const pswim_scenario s = to_c(sc.cfg);
+    pswim_ctx* ctx = Contexts::get(device, &s);
+    const pintswim::parareal::Vec in = pintswim::pack_state(rods);
+    std::vector<pintswim::Vec3> out(in.size() / 12);
+    throw_for(pswim_lj_forces_host(ctx, in.data(), reinterpret_cast<double*>(out.data())), pswim_last_error(ctx));
+    return out;
+}
+
 // pintswim::propagate on the device (state in, state out; packed via pack_state).
 inline pintswim::SystemState propagate(const pintswim::SystemState& state, double t0, double t1,
                                        const pintswim::StepperConfig& cfg, const pintswim::Scenario& sc,

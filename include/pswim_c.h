@@ -148,6 +148,8 @@ int pswim_rod_loads(pswim_ctx* ctx, const double* d_state, double t, double* d_f
 
 /* lj_repulsion, src/rod.cpp:124-174 (raw pair forces, N x 3, before the 1/ds factor). */
 int pswim_lj_forces(pswim_ctx* ctx, const double* d_state, double* d_forces);
+/* Host-buffer form (packed 12 N state in, N x 3 forces out). */
+int pswim_lj_forces_host(pswim_ctx* ctx, const double* h_state, double* h_forces);
 
 /* LJ pair search used by pswim_lj_forces and rhs: 0 = auto (all-pairs tiles below 2048
  * nodes, hashed cell list of side 2^(1/6) sigma above), 1 = all-pairs, 2 = cell list.

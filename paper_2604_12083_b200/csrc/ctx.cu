@@ -460,6 +460,20 @@ int pswim_lj_forces(pswim_ctx* ctx, const double* d_state, double* d_forces) {
     return PSWIM_OK;
 }
 
+int pswim_lj_forces_host(pswim_ctx* ctx, const double* h_state, double* h_forces) {
+    if (!ctx) return PSWIM_EINVAL;
+    if (!ctx->has_scenario) return ctx->fail(PSWIM_EINVAL, "lj: context has no scenario");
+    int rc = ctx->use();
+    if (rc) return rc;
+    const size_t n = static_cast<size_t>(ctx->rp.rods * ctx->rp.m);
+    if ((rc = ctx->ensure(&ctx->h_in, &ctx->cap_in, 12 * n))) return rc;
+    if ((rc = ctx->ensure(&ctx->h_o1, &ctx->cap_o1, 3 * n))) return rc;
+    CK(cudaMemcpyAsync(ctx->h_in, h_state, 12 * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    if ((rc = pswim_lj_forces(ctx, ctx->h_in, ctx->h_o1))) return rc;
+    CK(cudaMemcpyAsync(h_forces, ctx->h_o1, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    return ctx->sync();
+}
+
 int pswim_rhs(pswim_ctx* ctx, const double* d_state, double t, const double* d_ef, const double* d_en, double* d_u,
               double* d_omega) {
     if (!ctx) return PSWIM_EINVAL;
