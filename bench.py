@@ -264,7 +264,7 @@ def run_ours(args) -> None:
         e2e_t.append(time.perf_counter() - t0)
     e2e_s = reduce_max(sum(e2e_t) / len(e2e_t), dev)
     e2e_value = world * n * n / e2e_s / 1e9
-    h2d = 4 * n * 3 * 8
+    h2d = 3 * n * 3 * 8  # positions (targets = sources: copied once), f, n
     d2h = 2 * n * 3 * 8
 
     # --- roofline of the dominant kernel ---

@@ -395,11 +395,14 @@ int pswim_mrs_velocities_host(pswim_ctx* ctx, const double* h_t, int64_t nt, con
     if ((rc = ctx->ensure(&ctx->h_c, &ctx->cap_c, s3 > 0 ? s3 : 1))) return rc;
     if ((rc = ctx->ensure(&ctx->h_o1, &ctx->cap_o1, t3 > 0 ? t3 : 1))) return rc;
     if ((rc = ctx->ensure(&ctx->h_o2, &ctx->cap_o2, t3 > 0 ? t3 : 1))) return rc;
-    CK(cudaMemcpyAsync(ctx->h_in, h_t, t3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    // targets = sources (the rhs call, propagators.cpp:87): one copy serves both
+    const bool same = h_t == h_s && nt == ns;
+    if (!same) CK(cudaMemcpyAsync(ctx->h_in, h_t, t3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_a, h_s, s3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_b, h_f, s3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_c, h_n, s3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    rc = pswim_mrs_velocities(ctx, ctx->h_in, nt, ctx->h_a, ctx->h_b, ctx->h_c, ns, kp, ctx->h_o1, ctx->h_o2);
+    rc = pswim_mrs_velocities(ctx, same ? ctx->h_a : ctx->h_in, nt, ctx->h_a, ctx->h_b, ctx->h_c, ns, kp, ctx->h_o1,
+                              ctx->h_o2);
     if (rc) return rc;
     CK(cudaMemcpyAsync(h_u, ctx->h_o1, t3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(h_w, ctx->h_o2, t3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
