@@ -109,13 +109,16 @@ def dist_env():
     return world, rank, local
 
 
+WIRE = "nccl"  # "gloo": test mode -- ranks may share a GPU, transports staged over gloo
+
+
 def reduce_max(value: float, device=None) -> float:
     import torch
     import torch.distributed as dist
 
     if not (dist.is_available() and dist.is_initialized()):
         return value
-    t = torch.tensor([value], dtype=torch.float64, device=device)
+    t = torch.tensor([value], dtype=torch.float64, device=device if WIRE == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -174,8 +177,13 @@ def run_ours(args) -> None:
     import torch.distributed as dist
 
     world, rank, local = dist_env()
+    if WIRE != "nccl":
+        local = local % torch.cuda.device_count()  # test mode: ranks may share a GPU
     if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if WIRE == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
@@ -397,7 +405,7 @@ def time_steps_leg(args, world, rank, local, dev):
     fine_steps, coarse_steps = args.fine_steps, max(1, args.fine_steps // 10)
     plan = pr.ParallelPlan(t0=0.0, horizon=world * fine_steps * 1e-6, intervals=world, workers=world,
                            max_iterations=args.parareal_iters, tolerance=1e-300, mode=pr.PIPELINED)
-    tr = pr.nccl_transport(local)
+    tr = _transport(local)
     try:
         pr.run_sliced_rank(plan, sc, fine_steps, coarse_steps, x0, local, transport=tr)  # warm-up
         barrier()
@@ -436,7 +444,7 @@ def hybrid_leg(args, sc, x0, local, dev, world, members):
     slices = world // members
     tg, sg = pr.hybrid_groups(world, members)
     groups = tg + sg + sg  # time, space (coarse), space (fine): every rank creates them in this order
-    trs = pr.nccl_group_transports(local, groups)
+    trs = _group_transports(local, groups)
     q, p = rank % members, rank // members
     t_tr, c_tr, f_tr = trs[q], trs[len(tg) + p], trs[len(tg) + len(sg) + p]
     fine_steps, coarse_steps = args.fine_steps, max(1, args.fine_steps // 10)
@@ -602,10 +610,46 @@ def _hbm_peak() -> float:
         return 6650.0  # B200_PROFILING.md fallback
 
 
+_STAGED = {}  # transport pointer address -> StagedTransport (test-mode wire)
+
+
+def _transport(local):
+    """The rank's device transport over the whole world: NCCL, or (test mode) staged gloo."""
+    from paper_2604_12083_b200 import parareal as pr
+
+    if WIRE == "nccl":
+        return pr.nccl_transport(local)
+    st = pr.StagedTransport(local)
+    _STAGED[C.addressof(st.ptr.contents)] = st
+    return st.ptr
+
+
+def _group_transports(local, groups):
+    import torch.distributed as dist
+
+    from paper_2604_12083_b200 import parareal as pr
+
+    if WIRE == "nccl":
+        return pr.nccl_group_transports(local, groups)
+    out = {}
+    rank = dist.get_rank()
+    for gi, g in enumerate(groups):
+        pg = dist.new_group(g)  # collective over the world, every rank in the same order
+        if rank in g:
+            st = pr.StagedTransport(local, pg)
+            _STAGED[C.addressof(st.ptr.contents)] = st
+            out[gi] = st.ptr
+    return out
+
+
 def _lib_destroy(tr):
     from paper_2604_12083_b200 import _lib
 
-    _lib.lib().pswim_nccl_transport_destroy(tr)
+    st = _STAGED.pop(C.addressof(tr.contents), None)
+    if st is not None:
+        st.close()
+    else:
+        _lib.lib().pswim_nccl_transport_destroy(tr)
 
 
 def main():
@@ -619,7 +663,11 @@ def main():
     ap.add_argument("--parareal-iters", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (profiling runs)")
     ap.add_argument("--no-steps", action="store_true", help="skip the time-step leg")
+    ap.add_argument("--wire", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 transport; gloo = test mode (ranks may share one GPU, staged host transports)")
     args = ap.parse_args()
+    global WIRE
+    WIRE = args.wire
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

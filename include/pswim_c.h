@@ -294,6 +294,13 @@ typedef struct pswim_transport {
     int (*allgather)(void* user, const double* send, double* recv, int64_t count, void* stream);
 } pswim_transport;
 
+/* Device-buffer transport over a host-buffer wire (e.g. a torch.distributed gloo group or a
+ * socket): each call drains the stream, stages through pinned host memory and calls the
+ * wire's callbacks with host pointers.  For ranks that cannot use NCCL (several ranks on one
+ * GPU); NCCL (pswim_nccl_transport_create) is the NVLink path.  The wire struct is copied. */
+pswim_transport* pswim_staged_transport_create(const pswim_transport* host_wire, int device);
+void pswim_staged_transport_destroy(pswim_transport* t);
+
 /* Rank driver: rank p owns interval p+1 of a plan with intervals == world.  Runs the
  * pipelined (or regular) Parareal recurrence of src/parareal.cpp:58-89 with one state
  * hand-off per iteration to rank p+1 and one allreduce(max) of the iteration metric.

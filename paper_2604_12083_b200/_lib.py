@@ -130,6 +130,8 @@ SIGNATURES = {
     "pswim_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "pswim_nccl_transport_create": (C.POINTER(Transport), [C.POINTER(C.c_uint8), _i32, _i32, C.c_int]),
     "pswim_nccl_transport_destroy": (None, [C.POINTER(Transport)]),
+    "pswim_staged_transport_create": (C.POINTER(Transport), [C.POINTER(Transport), C.c_int]),
+    "pswim_staged_transport_destroy": (None, [C.POINTER(Transport)]),
     "pswim_threads_transports_create": (C.POINTER(Transport), [C.c_int32, C.POINTER(C.c_int), _i64, C.c_int32]),
     "pswim_threads_transports_destroy": (None, [C.POINTER(Transport)]),
     "pswim_propagate_sharded": (C.c_int, [_vp, C.POINTER(Transport), _vp, C.c_double, C.c_double, C.c_int, _i64,

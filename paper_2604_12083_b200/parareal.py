@@ -289,7 +289,9 @@ class TorchTransport:
 
         self.dist = dist
         self.group = group
-        rank, world = dist.get_rank(), dist.get_world_size()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        # peers are group ranks; torch.distributed point-to-point calls take global ranks
+        self._global = [dist.get_global_rank(group, r) if group is not None else r for r in range(world)]
         self._send = _lib.SEND_FN(self._send_cb)
         self._recv = _lib.RECV_FN(self._recv_cb)
         self._red = _lib.ALLREDUCE_FN(self._red_cb)
@@ -301,7 +303,7 @@ class TorchTransport:
 
         try:
             t = torch.from_numpy(np.ctypeslib.as_array(buf, shape=(length,)).copy())
-            self.dist.send(t, dst=peer, group=self.group)
+            self.dist.send(t, dst=self._global[peer], group=self.group)
             return 0
         except Exception:
             return 7
@@ -311,7 +313,7 @@ class TorchTransport:
 
         try:
             t = torch.empty(length, dtype=torch.float64)
-            self.dist.recv(t, src=peer, group=self.group)
+            self.dist.recv(t, src=self._global[peer], group=self.group)
             np.ctypeslib.as_array(buf, shape=(length,))[:] = t.numpy()
             return 0
         except Exception:
@@ -322,7 +324,7 @@ class TorchTransport:
 
         try:
             t = torch.from_numpy(np.ctypeslib.as_array(send, shape=(count,)).copy())
-            out = [torch.empty(count, dtype=torch.float64) for _ in range(self.dist.get_world_size())]
+            out = [torch.empty(count, dtype=torch.float64) for _ in range(self.dist.get_world_size(self.group))]
             self.dist.all_gather(out, t, group=self.group)
             np.ctypeslib.as_array(recv, shape=(count * len(out),))[:] = torch.cat(out).numpy()
             return 0
@@ -368,6 +370,25 @@ def run_sliced_rank_host(plan: ParallelPlan, coarse, fine, x0, metric=None, refe
                                     out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep))
     _lib.raise_for(rc, "parareal rank driver failed")
     return RankResult(out, _finish(rep, et, ea, ref is not None))
+
+
+class StagedTransport:
+    """Device-buffer transport over a torch.distributed host wire (gloo), staged through
+    pinned memory (pswim_staged_transport_create): the GPU rank drivers with several ranks on
+    one GPU, where NCCL refuses duplicate devices.  ``ptr`` is the pswim_transport*."""
+
+    def __init__(self, device: int, group=None):
+        L = _lib.lib()
+        self.wire = TorchTransport(group)
+        self.ptr = L.pswim_staged_transport_create(C.byref(self.wire.c), int(device))
+        if not self.ptr:
+            raise _lib.PswimError(7, "pswim_staged_transport_create failed")
+        self.lib = L
+
+    def close(self):
+        if self.ptr:
+            self.lib.pswim_staged_transport_destroy(self.ptr)
+            self.ptr = None
 
 
 def nccl_transport(device: int):

@@ -1,0 +1,44 @@
+"""The bench's N > 1 code path end to end on one B200: torchrun with 2 and 4 ranks sharing
+cuda:0, `--wire gloo` (NCCL refuses two ranks on one device, so the slice hand-offs,
+all-gathers and metric allreduce go through pswim_staged_transport over gloo).  Exercises
+the time-sliced Parareal leg, the space-parallel legs (collective and fused peer all-gather
+over CUDA IPC) and, at 4 ranks, the hybrid space x time leg, and checks the JSON line."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_bench_multirank_gloo_wire(gpu, world):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "bench.py"),
+           "--gpus", str(world), "--steps", "3", "--warmup", "3", "--wire", "gloo", "--fine-steps", "4",
+           "--no-cpu"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
+    d = json.loads(lines[-1])
+    assert d["n_gpus"] == world and d["value"] > 0
+    ts = d["time_steps"]
+    assert "error" not in ts and ts["value"] > 0 and ts["config"]["intervals"] == world, ts
+    sp = ts["space_parallel"]
+    assert "error" not in sp and sp["value"] > 0, sp
+    assert "error" not in sp["fused_peer_allgather"], sp
+    if world >= 4:
+        hy = ts["hybrid_space_time"]
+        assert "error" not in hy and hy["value"] > 0 and hy["config"]["iterations"] == 1, hy
