@@ -8,7 +8,7 @@
 //   lj_kernel         lj_repulsion (src/rod.cpp:124-174) as a per-node all-pairs sum.
 //   advance_kernel    advance_state (src/propagators.cpp:93-124) + reorthonormalize
 //                     (src/rod.cpp:176-195), one thread per node.
-//   sqrt_batched      sqrt_rotation over a batch (rotation.cpp:91-107), smem-staged.
+//   sqrt_wtma_kernel  sqrt_rotation over a batch (rotation.cpp:91-107), per-warp TMA rings.
 //   metric / correct  rod_position_metric (io.cpp:49-68), corrected (parareal.cpp:47-54).
 #include <algorithm>
 #include <cmath>
@@ -285,88 +285,70 @@ rod_loads_wtma_kernel(RodArgs p, int total, const double* __restrict__ state, do
 }
 
 // ---------------------------------------------------------------------------------------
-// batched sqrt_rotation, persistent TMA-bulk pipeline: chunks of 256 row-major matrices
-// (18 KiB) stream global -> shared with cp.async.bulk into a 3-stage ring (mbarrier
-// completion), one thread per matrix computes in registers and writes the square root back
-// into the same stage, which leaves with one cp.async.bulk shared -> global store.  A ragged
-// tail chunk (count % 256) and unaligned pointers take the plain-load path.
+// batched sqrt_rotation (rotation.cpp:91-107 over a batch of row-major matrices)
 // ---------------------------------------------------------------------------------------
 constexpr int kSqrtBlock = 256;
-constexpr int kSqrtStages = 3;
-constexpr uint32_t kSqrtChunkBytes = kSqrtBlock * 9 * sizeof(double);
 
-__device__ __forceinline__ void sqrt_chunk_compute(double* b, int nmat) {
-    m33 r;
-    const bool active = threadIdx.x < nmat;
-    if (active) {
-#pragma unroll
-        for (int e = 0; e < 9; ++e) r.m[e] = b[9 * threadIdx.x + e];
-    }
-    __syncthreads();
-    if (active) {
-        const m33 s = sqrt_rotation(r);
-#pragma unroll
-        for (int e = 0; e < 9; ++e) b[9 * threadIdx.x + e] = s.m[e];
-    }
-}
+// Each warp streams chunks of 32 matrices (2304 B) through its own
+// kSqrtWarpStages-deep TMA ring (one mbarrier per stage, issued by lane 0), computes one
+// matrix per lane in place, and stores the chunk back with one bulk copy.  No CTA barrier:
+// a lane only touches its own 72 bytes until the warp-level fence + __syncwarp before the
+// store.  A stage is refilled one iteration after its store was issued
+// (cp.async.bulk.wait_group.read 1), so lane 0 never waits for the store it just issued.
+constexpr int kSqrtWarpStages = 4;
+constexpr uint32_t kSqrtWarpChunkBytes = 32 * 9 * sizeof(double);
 
-__global__ void __launch_bounds__(kSqrtBlock, 3)
-sqrt_tma_kernel(const double* __restrict__ r9, int64_t count, double* __restrict__ s9) {
+__global__ void __launch_bounds__(256, 3)
+sqrt_wtma_kernel(const double* __restrict__ r9, int64_t nwchunks, double* __restrict__ s9) {
     extern __shared__ __align__(128) unsigned char smem[];
-    double* stage[kSqrtStages];
-#pragma unroll
-    for (int s = 0; s < kSqrtStages; ++s) stage[s] = reinterpret_cast<double*>(smem + s * kSqrtChunkBytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSqrtStages * kSqrtChunkBytes);
-    const int64_t nchunks = (count + kSqrtBlock - 1) / kSqrtBlock;
-    const int64_t nfull = count / kSqrtBlock;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kSqrtStages; ++s) mbar_init(&full[s], 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, warps = blockDim.x >> 5;
+    double* ring = reinterpret_cast<double*>(smem) + (size_t)warp * kSqrtWarpStages * 32 * 9;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)warps * kSqrtWarpStages * kSqrtWarpChunkBytes) +
+                     warp * kSqrtWarpStages;
+    const int64_t wstride = (int64_t)gridDim.x * warps, w0 = (int64_t)blockIdx.x * warps + warp;
+    if (lane == 0) {
+        for (int s = 0; s < kSqrtWarpStages; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kSqrtStages; ++s) {
-            const int64_t c = blockIdx.x + (int64_t)s * gridDim.x;
-            if (c < nfull) {
-                mbar_expect_tx(&full[s], kSqrtChunkBytes);
-                bulk_load(stage[s], r9 + 9 * kSqrtBlock * c, kSqrtChunkBytes, &full[s]);
+        for (int s = 0; s < kSqrtWarpStages; ++s) {
+            const int64_t c = w0 + s * wstride;
+            if (c < nwchunks) {
+                mbar_expect_tx(&bars[s], kSqrtWarpChunkBytes);
+                bulk_load(ring + s * 32 * 9, r9 + 9 * 32 * c, kSqrtWarpChunkBytes, &bars[s]);
             }
         }
     }
-    for (int64_t k = 0;; ++k) {
-        const int64_t c = blockIdx.x + k * gridDim.x;
-        if (c >= nchunks) break;
-        const int s = (int)(k % kSqrtStages);
-        double* b = stage[s];
-        if (c < nfull) {
-            mbar_wait(&full[s], (uint32_t)((k / kSqrtStages) & 1));
-            sqrt_chunk_compute(b, kSqrtBlock);
-            fence_proxy_async_smem();
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                bulk_store(s9 + 9 * kSqrtBlock * c, b, kSqrtChunkBytes);
-                bulk_commit();
-                const int64_t cn = blockIdx.x + (k + kSqrtStages) * gridDim.x;
-                if (cn < nfull) {
-                    bulk_wait_read<0>();  // the stage's outgoing store has left shared memory
-                    mbar_expect_tx(&full[s], kSqrtChunkBytes);
-                    bulk_load(b, r9 + 9 * kSqrtBlock * cn, kSqrtChunkBytes, &full[s]);
+    __syncwarp();
+    int i = 0;
+    for (int64_t c = w0; c < nwchunks; c += wstride, ++i) {
+        const int s = i % kSqrtWarpStages;
+        double* b = ring + s * 32 * 9;
+        mbar_wait(&bars[s], (uint32_t)((i / kSqrtWarpStages) & 1));
+        m33 r;
+#pragma unroll
+        for (int e = 0; e < 9; ++e) r.m[e] = b[9 * lane + e];
+        const m33 q = sqrt_rotation(r);
+#pragma unroll
+        for (int e = 0; e < 9; ++e) b[9 * lane + e] = q.m[e];
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            bulk_store(s9 + 9 * 32 * c, b, kSqrtWarpChunkBytes);
+            bulk_commit();
+            if (i > 0) {
+                // refill the previous iteration's stage once its store has left shared memory
+                const int sp = (i - 1) % kSqrtWarpStages;
+                const int64_t cn = c - wstride + kSqrtWarpStages * wstride;
+                if (cn < nwchunks) {
+                    bulk_wait_read<1>();
+                    mbar_expect_tx(&bars[sp], kSqrtWarpChunkBytes);
+                    bulk_load(ring + sp * 32 * 9, r9 + 9 * 32 * cn, kSqrtWarpChunkBytes, &bars[sp]);
                 }
             }
-        } else {
-            const int nmat = (int)(count - c * kSqrtBlock);
-            __syncthreads();
-            for (int e = threadIdx.x; e < 9 * nmat; e += kSqrtBlock) b[e] = r9[9 * kSqrtBlock * c + e];
-            __syncthreads();
-            sqrt_chunk_compute(b, nmat);
-            __syncthreads();
-            for (int e = threadIdx.x; e < 9 * nmat; e += kSqrtBlock) s9[9 * kSqrtBlock * c + e] = b[e];
         }
     }
-    if (threadIdx.x == 0) bulk_wait<0>();
+    if (lane == 0) bulk_wait<0>();
 }
 
-// Fallback for pointers that are not 16-byte aligned.
 __global__ void __launch_bounds__(kSqrtBlock)
 sqrt_plain_kernel(const double* __restrict__ r9, int64_t count, double* __restrict__ s9) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -503,7 +485,7 @@ void rod_preload() {
     cudaFuncGetAttributes(&a, rod_loads_kernel);
     cudaFuncGetAttributes(&a, rod_loads_wtma_kernel<kRodStages>);
     cudaFuncGetAttributes(&a, lj_kernel);
-    cudaFuncGetAttributes(&a, sqrt_tma_kernel);
+    cudaFuncGetAttributes(&a, sqrt_wtma_kernel);
     cudaFuncGetAttributes(&a, sqrt_plain_kernel);
     cudaFuncGetAttributes(&a, metric_kernel);
     cudaFuncGetAttributes(&a, correct_kernel);
@@ -541,17 +523,22 @@ cudaError_t sqrt_batched_launch(const double* r9, int64_t count, double* s9, cud
         sqrt_plain_kernel<<<grid_for(count, kSqrtBlock), kSqrtBlock, 0, st>>>(r9, count, s9);
         return cudaGetLastError();
     }
-    const size_t smem = kSqrtStages * kSqrtChunkBytes + kSqrtStages * sizeof(uint64_t);
+    // per-warp TMA rings over the whole 32-matrix chunks, plain tail
+    const int64_t nw = count / 32;
+    const size_t wsmem = 8 * (size_t)kSqrtWarpStages * (kSqrtWarpChunkBytes + sizeof(uint64_t));
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(sqrt_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(sqrt_wtma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem);
         configured = true;
     }
-    const int64_t nchunks = (count + kSqrtBlock - 1) / kSqrtBlock;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sqrt_tma_kernel, kSqrtBlock, smem);
-    const int64_t grid = std::min<int64_t>(nchunks, (int64_t)num_sms() * std::max(per_sm, 1));  // persistent
-    sqrt_tma_kernel<<<(unsigned)grid, kSqrtBlock, smem, st>>>(r9, count, s9);
+    if (nw > 0) {
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sqrt_wtma_kernel, 256, wsmem);
+        const int64_t grid = std::min<int64_t>((nw + 7) / 8, (int64_t)num_sms() * std::max(per_sm, 1));
+        sqrt_wtma_kernel<<<(unsigned)grid, 256, wsmem, st>>>(r9, nw, s9);
+    }
+    const int64_t tail = count - 32 * nw;
+    if (tail > 0) sqrt_plain_kernel<<<1, kSqrtBlock, 0, st>>>(r9 + 9 * 32 * nw, tail, s9 + 9 * 32 * nw);
     return cudaGetLastError();
 }
 
