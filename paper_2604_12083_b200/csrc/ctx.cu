@@ -129,6 +129,7 @@ int pswim_ctx::mrs(const double* tgt, int64_t nt, const double* src, const doubl
 
 int pswim_ctx::lj(const double* state, double* out) {
     const int64_t total = rp.rods * rp.m;
+    if (total >= ((int64_t)1 << 31) / 12) return fail(PSWIM_EINVAL, "lj: more nodes than the 32-bit pair kernels index");
     const bool cells = lj_mode == 2 || (lj_mode == 0 && total >= kLjCellsMinNodes);
     const cudaError_t e = cells ? lj_cells_launch(rp, state, out, &lj_work, stream) : lj_launch(rp, state, out, stream);
     if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("lj: ") + cudaGetErrorString(e));
@@ -542,12 +543,15 @@ int pswim_fused_profile(pswim_ctx* ctx, const double* d_in, double t0, double t1
     const size_t bytes = sizeof(double) * 12 * static_cast<size_t>(ctx->rp.rods * ctx->rp.m);
     unsigned long long* prof = nullptr;
     CK(cudaMalloc(&prof, sizeof(unsigned long long) * kFusedPhases));
-    CK(cudaMemsetAsync(prof, 0, sizeof(unsigned long long) * kFusedPhases, ctx->stream));
-    if (d_in != d_out) CK(cudaMemcpyAsync(d_out, d_in, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
-    CK(fused_propagate_launch(ctx->rp, d_out, steps, t0, dt, scheme, ctx->d_flags, ctx->stream, prof));
-    CK(cudaMemcpyAsync(h_cycles7, prof, sizeof(unsigned long long) * kFusedPhases, cudaMemcpyDeviceToHost,
-                       ctx->stream));
-    rc = ctx->sync();
+    cudaError_t e = cudaMemsetAsync(prof, 0, sizeof(unsigned long long) * kFusedPhases, ctx->stream);
+    if (e == cudaSuccess && d_in != d_out)
+        e = cudaMemcpyAsync(d_out, d_in, bytes, cudaMemcpyDeviceToDevice, ctx->stream);
+    if (e == cudaSuccess) e = fused_propagate_launch(ctx->rp, d_out, steps, t0, dt, scheme, ctx->d_flags, ctx->stream, prof);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(h_cycles7, prof, sizeof(unsigned long long) * kFusedPhases, cudaMemcpyDeviceToHost,
+                            ctx->stream);
+    rc = e == cudaSuccess ? ctx->sync() : ctx->fail(PSWIM_ECUDA, std::string("fused_profile: ") + cudaGetErrorString(e));
+    cudaStreamSynchronize(ctx->stream);
     cudaFree(prof);
     return rc;
 }
