@@ -194,6 +194,12 @@ int pswim_set_fused(pswim_ctx* ctx, int enable);
 int pswim_fused_profile(pswim_ctx* ctx, const double* d_in, double t0, double t1, int scheme,
                         int64_t steps_per_interval, double* d_out, uint64_t* h_cycles7);
 
+/* CUDA-graph replay of the per-step kernels for propagations of >= 32 steps of systems of
+ * <= 8192 nodes outside the fused path (one graph launch per 32 steps, times read from
+ * device memory; larger systems are not launch bound and run the plain loop): bitwise
+ * identical to the launch-per-kernel loop.  Enabled by default; returns the previous state. */
+int pswim_set_graphs(pswim_ctx* ctx, int enable);
+
 /* Host-buffer propagate (e2e boundary: H2D, propagate, D2H). */
 int pswim_propagate_host(pswim_ctx* ctx, const double* h_in, double t0, double t1, int scheme,
                          int64_t steps_per_interval, double dt, double* h_out);

@@ -107,6 +107,7 @@ SIGNATURES = {
     "pswim_propagate_host": (C.c_int, [_vp, _dp, C.c_double, C.c_double, C.c_int, _i64, C.c_double, _dp]),
     "pswim_set_fused": (C.c_int, [_vp, C.c_int]),
     "pswim_set_lj_mode": (C.c_int, [_vp, C.c_int]),
+    "pswim_set_graphs": (C.c_int, [_vp, C.c_int]),
     "pswim_lj_forces_host": (C.c_int, [_vp, _dp, _dp]),
     "pswim_fused_profile": (C.c_int, [_vp, _vp, C.c_double, C.c_double, C.c_int, C.c_int64, _vp,
                                       C.POINTER(C.c_uint64)]),

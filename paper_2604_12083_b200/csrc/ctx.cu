@@ -136,7 +136,8 @@ int pswim_ctx::lj(const double* state, double* out) {
     return PSWIM_OK;
 }
 
-int pswim_ctx::rhs(const double* state, double t, const double* ef, const double* en, double* u, double* w) {
+int pswim_ctx::rhs(const double* state, double t, const double* ef, const double* en, double* u, double* w,
+                   const double* tdev) {
     if (!has_scenario) return fail(PSWIM_EINVAL, "rhs: context has no scenario");
     if (sc.wall_mode == 1) return fail(PSWIM_EUNSUPPORTED_WALL, "stokes: image_wall correction is not implemented; use free_space");
     stage_begin(0);
@@ -146,7 +147,7 @@ int pswim_ctx::rhs(const double* state, double t, const double* ef, const double
         if (rc) return rc;
     }
     cudaError_t e = rod_loads_launch(rp, state, t, nullptr, d_f, d_n, nullptr, nullptr, lj ? d_lj : nullptr, ef, en,
-                                     d_flags, stream);
+                                     d_flags, stream, tdev);
     if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("rod_loads_launch: ") + cudaGetErrorString(e));
     stage_end();
     stage_begin(1);
@@ -165,14 +166,14 @@ int pswim_ctx::advance(const double* state, const double* u, const double* w, do
     return PSWIM_OK;
 }
 
-int pswim_ctx::step(int scheme, const double* state, double t, double dt, double* out) {
+int pswim_ctx::step(int scheme, const double* state, double t, double dt, double* out, const double* tdev2) {
     // step_euler / step_rk2, propagators.cpp:126-133.  In-place safe (advance is per node).
-    int rc = rhs(state, t, nullptr, nullptr, d_u, d_w);
+    int rc = rhs(state, t, nullptr, nullptr, d_u, d_w, tdev2);
     if (rc) return rc;
     if (scheme == PSWIM_EULER) return advance(state, d_u, d_w, dt, out);
     rc = advance(state, d_u, d_w, 0.5 * dt, d_mid);
     if (rc) return rc;
-    rc = rhs(d_mid, t + 0.5 * dt, nullptr, nullptr, d_u, d_w);
+    rc = rhs(d_mid, t + 0.5 * dt, nullptr, nullptr, d_u, d_w, tdev2 ? tdev2 + 1 : nullptr);
     if (rc) return rc;
     return advance(state, d_u, d_w, dt, out);
 }
@@ -225,6 +226,10 @@ int pswim_ctx::propagate_async(const double* d_in, double t0, double t1, int sch
         if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("fused_propagate: ") + cudaGetErrorString(e));
         return PSWIM_OK;
     }
+    // graphs pay where kernel launches are a visible share of a step (mid-size systems); large
+    // systems would only add the one-off capture to the first interval
+    if (graphs_on && !timing_on && steps >= kGraphSteps && rp.rods * rp.m <= kGraphMaxNodes)
+        return propagate_graph(t0, scheme, steps, dt, d_out);
     double t = t0;
     for (int64_t i = 0; i < steps; ++i) {
         rc = step(scheme, d_out, t, dt, d_out);
@@ -232,6 +237,76 @@ int pswim_ctx::propagate_async(const double* d_in, double t0, double t1, int sch
         t += dt;  // propagators.cpp:159
     }
     return PSWIM_OK;
+}
+
+int pswim_ctx::propagate_graph(double t0, int scheme, int64_t steps, double dt, double* d_out) {
+    // The same kernels with the same arguments as the step loop (bitwise identical), replayed
+    // from one captured graph of kGraphSteps steps: one launch instead of 6 (RK2) or 3 (Euler)
+    // per step.  Times come from device memory: t_i by the reference's accumulation t += dt
+    // (propagators.cpp:159) on the host, and t_i + dt/2, per step.
+    const size_t n12 = 12 * static_cast<size_t>(rp.rods * rp.m);
+    int rc = ensure(&d_gstate, &cap_gstate, n12);
+    if (rc) return rc;
+    if ((rc = ensure(&d_times_all, &cap_times_all, 2 * static_cast<size_t>(steps)))) return rc;
+    if (!d_times && cudaMalloc(&d_times, 2 * kGraphSteps * sizeof(double)) != cudaSuccess)
+        return fail(PSWIM_ECUDA, "graph: cudaMalloc times");
+    if (!times_done && cudaEventCreateWithFlags(&times_done, cudaEventDisableTiming) != cudaSuccess)
+        return fail(PSWIM_ECUDA, "graph: event");
+    // host times, staged through pinned memory (wait for the previous upload to have read it)
+    cudaEventSynchronize(times_done);
+    if (cap_h_times < 2 * static_cast<size_t>(steps)) {
+        if (h_times) cudaFreeHost(h_times);
+        h_times = nullptr;
+        cap_h_times = 0;
+        if (cudaMallocHost(&h_times, 2 * steps * sizeof(double)) != cudaSuccess)
+            return fail(PSWIM_ECUDA, "graph: pinned times");
+        cap_h_times = 2 * static_cast<size_t>(steps);
+    }
+    double t = t0;
+    for (int64_t i = 0; i < steps; ++i) {
+        h_times[2 * i] = t;
+        h_times[2 * i + 1] = t + 0.5 * dt;
+        t += dt;  // propagators.cpp:159
+    }
+    cudaError_t e = cudaMemcpyAsync(d_times_all, h_times, 2 * steps * sizeof(double), cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaEventRecord(times_done, stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_gstate, d_out, n12 * sizeof(double), cudaMemcpyDeviceToDevice, stream);
+    if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("graph: staging: ") + cudaGetErrorString(e));
+    // (re)capture when the step or any workspace it touches changed
+    const void* key[4] = {d_scratch, d_counters, lj_work.key, d_mid};
+    const bool stale = !graph_exec || graph_scheme != scheme || graph_dt != dt ||
+                       std::memcmp(key, graph_key, sizeof key) != 0;
+    if (stale) {
+        if (graph_exec) cudaGraphExecDestroy(graph_exec);
+        graph_exec = nullptr;
+        cudaGraph_t g = nullptr;
+        if ((e = cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed)) != cudaSuccess)
+            return fail(PSWIM_ECUDA, std::string("graph: capture: ") + cudaGetErrorString(e));
+        for (int i = 0; i < kGraphSteps && rc == PSWIM_OK; ++i)
+            rc = step(scheme, d_gstate, 0.0, dt, d_gstate, d_times + 2 * i);
+        e = cudaStreamEndCapture(stream, &g);
+        if (rc) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&graph_exec, g, 0);
+        if (g) cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("graph: instantiate: ") + cudaGetErrorString(e));
+        graph_scheme = scheme;
+        graph_dt = dt;
+        std::memcpy(graph_key, key, sizeof key);
+    }
+    const int64_t full = steps / kGraphSteps;
+    for (int64_t c = 0; c < full; ++c) {
+        e = cudaMemcpyAsync(d_times, d_times_all + 2 * kGraphSteps * c, 2 * kGraphSteps * sizeof(double),
+                            cudaMemcpyDeviceToDevice, stream);
+        if (e == cudaSuccess) e = cudaGraphLaunch(graph_exec, stream);
+        if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("graph: launch: ") + cudaGetErrorString(e));
+    }
+    for (int64_t i = full * kGraphSteps; i < steps; ++i)
+        if ((rc = step(scheme, d_gstate, h_times[2 * i], dt, d_gstate))) return rc;
+    e = cudaMemcpyAsync(d_out, d_gstate, n12 * sizeof(double), cudaMemcpyDeviceToDevice, stream);
+    return e == cudaSuccess ? PSWIM_OK : fail(PSWIM_ECUDA, "graph: copy out");
 }
 
 // ---- space-parallel MRS (sharded targets, velocity all-gather) ------------------------
@@ -287,6 +362,11 @@ pswim_ctx::~pswim_ctx() {
         if (p) cudaFree(p);
     if (d_counters) cudaFree(d_counters);
     lj_work.release();
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    for (double* p : {d_gstate, d_times, d_times_all})
+        if (p) cudaFree(p);
+    if (h_times) cudaFreeHost(h_times);
+    if (times_done) cudaEventDestroy(times_done);
     if (d_flags) cudaFree(d_flags);
     if (h_flags) cudaFreeHost(h_flags);
     if (stream) cudaStreamDestroy(stream);
@@ -554,6 +634,13 @@ int pswim_fused_profile(pswim_ctx* ctx, const double* d_in, double t0, double t1
     cudaStreamSynchronize(ctx->stream);
     cudaFree(prof);
     return rc;
+}
+
+int pswim_set_graphs(pswim_ctx* ctx, int enable) {
+    if (!ctx) return PSWIM_EINVAL;
+    const int prev = ctx->graphs_on ? 1 : 0;
+    ctx->graphs_on = enable != 0;
+    return prev;
 }
 
 int pswim_set_lj_mode(pswim_ctx* ctx, int mode) {

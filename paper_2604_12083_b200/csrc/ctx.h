@@ -59,13 +59,34 @@ struct pswim_ctx {
     int mrs(const double* tgt, int64_t nt, const double* src, const double* f, const double* n, int64_t ns,
             double eps, double mu, double* u, double* w, int pstride = 3);
     int lj(const double* state, double* out);  // lj_repulsion, rod.cpp:124-174
-    int rhs(const double* state, double t, const double* ef, const double* en, double* u, double* w);
+    // tdev / tdev2: optional device copies of t (and t + dt/2) read by the load kernels, so
+    // that a captured step replays at new times (CUDA graphs)
+    int rhs(const double* state, double t, const double* ef, const double* en, double* u, double* w,
+            const double* tdev = nullptr);
     int advance(const double* state, const double* u, const double* w, double dt, double* out);
-    int step(int scheme, const double* state, double t, double dt, double* out);
+    int step(int scheme, const double* state, double t, double dt, double* out, const double* tdev2 = nullptr);
     int resolve_steps(double t0, double t1, int64_t spi, double dtc, int64_t* steps, double* dt);
     // space: optional transport of a space group -> every rhs with the MRS sharded over it
     int propagate_async(const double* d_in, double t0, double t1, int scheme, int64_t spi, double dtc, double* d_out,
                         const pswim_transport* space = nullptr);
+
+    // CUDA-graph replay of the per-step kernel sequence (launch-bound mid-size systems):
+    // one captured graph runs kGraphSteps steps in place on d_gstate, the step times staged in
+    // d_times; rebuilt when scheme, dt or any workspace pointer changes.
+    static constexpr int kGraphSteps = 32;
+    static constexpr int64_t kGraphMaxNodes = 8192;
+    cudaGraphExec_t graph_exec = nullptr;
+    int graph_scheme = -1;
+    double graph_dt = 0.0;
+    const void* graph_key[4] = {nullptr, nullptr, nullptr, nullptr};
+    double* d_gstate = nullptr;
+    double* d_times = nullptr;      // 2 kGraphSteps (t, t + dt/2 per step)
+    double* d_times_all = nullptr;  // every step time of the current interval
+    double* h_times = nullptr;      // pinned staging
+    size_t cap_gstate = 0, cap_times_all = 0, cap_h_times = 0;
+    cudaEvent_t times_done = nullptr;  // the staging buffer's last upload finished
+    bool graphs_on = true;
+    int propagate_graph(double t0, int scheme, int64_t steps, double dt, double* d_out);
 
     // space-parallel (sharded MRS) path
     double* d_shard = nullptr;   // 6 S: this rank's (u, w) shard

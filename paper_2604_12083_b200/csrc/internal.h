@@ -82,10 +82,12 @@ struct RodParams {
     int64_t lj_excl = 4;
 };
 // internal + nodal loads: state (packed 12/node) -> pos, f, n (N x 3); optional segment
-// loads; extra loads added after LJ as rhs does (propagators.cpp:70-84).
+// loads; extra loads added after LJ as rhs does (propagators.cpp:70-84).  tdev (optional):
+// the time is read from device memory (CUDA-graph replays of the step loop).
 cudaError_t rod_loads_launch(const RodParams& p, const double* state, double t, double* pos, double* f,
                              double* n, double* seg_f, double* seg_n, const double* lj, const double* extra_f,
-                             const double* extra_n, unsigned* flags, cudaStream_t st);
+                             const double* extra_n, unsigned* flags, cudaStream_t st,
+                             const double* tdev = nullptr);
 cudaError_t lj_launch(const RodParams& p, const double* state, double* forces, cudaStream_t st);
 // Hashed cell-list LJ (lj_cells.cu): workspace grown on demand, owned by the context.
 struct LjWork {

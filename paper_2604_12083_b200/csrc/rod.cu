@@ -26,11 +26,13 @@ namespace {
 // internal_loads + nodal_loads
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
-rod_loads_kernel(RodArgs p, const double* __restrict__ state, double t, double* __restrict__ pos,
+rod_loads_kernel(RodArgs p, const double* __restrict__ state, double t0, const double* __restrict__ tdev,
+                 double* __restrict__ pos,
                  double* __restrict__ fo, double* __restrict__ no, double* __restrict__ seg_f,
                  double* __restrict__ seg_n, const double* __restrict__ lj, const double* __restrict__ extra_f,
                  const double* __restrict__ extra_n, unsigned* __restrict__ flags) {
     extern __shared__ double sh[];
+    const double t = tdev ? *tdev : t0;  // time from device memory inside CUDA graphs
     const int64_t m = p.m;
     double* xs = sh;            // m x 12 packed rod state
     double* seg = sh + 12 * m;  // (m-1) x 6: F, N per segment
@@ -204,7 +206,8 @@ constexpr uint32_t kTileBytes = kTileNodes * 96;
 
 template <int kStages>
 __global__ void __launch_bounds__(256, 2)
-rod_loads_wtma_kernel(RodArgs p, int total, const double* __restrict__ state, double t, double* __restrict__ pos,
+rod_loads_wtma_kernel(RodArgs p, int total, const double* __restrict__ state, double t0,
+                      const double* __restrict__ tdev, double* __restrict__ pos,
                       double* __restrict__ fo, double* __restrict__ no, const double* __restrict__ lj,
                       const double* __restrict__ extra_f, const double* __restrict__ extra_n,
                       unsigned* __restrict__ flags) {
@@ -216,6 +219,7 @@ rod_loads_wtma_kernel(RodArgs p, int total, const double* __restrict__ state, do
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + warps * kStages * kTileBytes) + warp * kStages;
     double* strain = reinterpret_cast<double*>(smem + warps * kStages * (kTileBytes + 8));  // m - 1 entries
     const int m = (int)p.m;
+    const double t = tdev ? *tdev : t0;  // time from device memory inside CUDA graphs
     for (int k = threadIdx.x; k + 1 < m; k += blockDim.x) strain[k] = rod_strain(p, k, t);
     const int wstride = gridDim.x * warps;
     const int w0 = blockIdx.x * warps + warp;
@@ -429,7 +433,7 @@ inline int num_sms() {
 
 cudaError_t rod_loads_launch(const RodParams& p, const double* state, double t, double* pos, double* f, double* n,
                              double* seg_f, double* seg_n, const double* lj, const double* extra_f,
-                             const double* extra_n, unsigned* flags, cudaStream_t st) {
+                             const double* extra_n, unsigned* flags, cudaStream_t st, const double* tdev) {
     const RodArgs a = rod_args(p);
     const size_t smem = sizeof(double) * (size_t)(12 * p.m + 6 * (p.m - 1));
     static bool configured = false;
@@ -452,12 +456,12 @@ cudaError_t rod_loads_launch(const RodParams& p, const double* state, double t, 
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rod_loads_wtma_kernel<kRodStages>, 256, sm);
         const int grid = (int)std::min<int64_t>((tiles + 7) / 8, (int64_t)num_sms() * std::max(per_sm, 1));
-        rod_loads_wtma_kernel<kRodStages><<<(unsigned)grid, 256, sm, st>>>(a, total, state, t, pos, f, n, lj, extra_f,
+        rod_loads_wtma_kernel<kRodStages><<<(unsigned)grid, 256, sm, st>>>(a, total, state, t, tdev, pos, f, n, lj, extra_f,
                                                                            extra_n, flags);
         return cudaGetLastError();
     }
     // segment loads requested, unaligned state or very long rods: one CTA per rod
-    rod_loads_kernel<<<(unsigned)p.rods, 256, smem, st>>>(a, state, t, pos, f, n, seg_f, seg_n, lj, extra_f, extra_n,
+    rod_loads_kernel<<<(unsigned)p.rods, 256, smem, st>>>(a, state, t, tdev, pos, f, n, seg_f, seg_n, lj, extra_f, extra_n,
                                                          flags);
     return cudaGetLastError();
 }

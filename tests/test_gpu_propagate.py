@@ -235,3 +235,36 @@ def test_fused_phase_profile(gpu):
     assert np.array_equal(out.cpu().numpy(), want)
     assert all(cyc[i] > 0 for i in (0, 1, 2, 3, 4, 5, 6))
     ctx.close()
+
+
+@pytest.mark.parametrize("kw,scheme,steps", [(dict(rod_count=3, nodes_per_rod=100), 1, 70),
+                                             (dict(rod_count=3, nodes_per_rod=100), 0, 64),
+                                             (dict(rod_count=4, nodes_per_rod=128, placement=1, lj_well_depth=0.01,
+                                                   seed=3, epsilon=0.08), 1, 33)])
+def test_graph_replay_bitwise_equals_step_loop(gpu, oracle, kw, scheme, steps):
+    """Propagations outside the fused path replay a captured CUDA graph of 32 steps (times
+    from device memory): bitwise equal to the launch-per-kernel loop, and to the oracle."""
+    from oracle.pyoracle import Scenario as OS
+    from paper_2604_12083_b200.device import Context
+    from paper_2604_12083_b200.propagators import StepperConfig, propagate
+    from paper_2604_12083_b200.scenario import build_initial_state
+
+    sc = scen(**kw)
+    x = build_initial_state(sc)
+    g, p = Context(0, sc), Context(0, sc)
+    assert g.lib.pswim_set_fused(g.handle, 0) == 0  # N > 256: not fused-eligible anyway
+    p.lib.pswim_set_fused(p.handle, 0)
+    assert p.lib.pswim_set_graphs(p.handle, 0) == 1
+    cfg = StepperConfig(0.0, scheme, steps)
+    t1 = steps * 1e-6
+    a = propagate(x, 0.0, t1, cfg, sc, ctx=g)
+    b = propagate(x, 0.0, t1, cfg, sc, ctx=p)
+    assert np.array_equal(a, b)
+    # a second interval reuses the captured graph at new times
+    a2 = propagate(a, t1, 2 * t1, cfg, sc, ctx=g)
+    b2 = propagate(b, t1, 2 * t1, cfg, sc, ctx=p)
+    assert np.array_equal(a2, b2)
+    want = oracle.propagate(OS.make(**kw), x, 0.0, t1, scheme, steps=steps)
+    assert oracle.position_metric(want, a) < 1e-10
+    g.close()
+    p.close()

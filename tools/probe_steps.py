@@ -11,10 +11,11 @@ from paper_2604_12083_b200.device import Context, dptr
 from paper_2604_12083_b200.scenario import ScenarioConfig, build_initial_state, make_scenario
 
 
-def rate(kw, steps, fused):
+def rate(kw, steps, fused, graphs=True):
     sc = make_scenario(ScenarioConfig(**kw))
     ctx = Context(0, sc)
     cs = ctx.lib.pswim_set_fused(ctx.handle, 1 if fused else 0)
+    ctx.lib.pswim_set_graphs(ctx.handle, 1 if graphs else 0)
     x = torch.as_tensor(build_initial_state(sc), device="cuda")
     out = torch.empty_like(x)
     L = ctx.lib
@@ -36,5 +37,12 @@ for kw, steps in [(dict(rod_count=1, nodes_per_rod=100), 20000), (dict(rod_count
     for fused in (True, False):
         r, cs = rate(kw, steps if fused else steps // 10, fused)
         print(f"{kw} fused={fused} cluster={cs}: {r:,.0f} RK2 steps/s")
-r, _ = rate(dict(rod_count=64, nodes_per_rod=256, epsilon=0.08), 100, False)
-print(f"64x256: {r:,.1f} RK2 steps/s")
+# the paper's benchmark sizes (4 / 12 / 25 rods x 51 nodes), per-step kernels
+for kw in (dict(rod_count=4, nodes_per_rod=51), dict(rod_count=12, nodes_per_rod=51),
+           dict(rod_count=25, nodes_per_rod=51), dict(rod_count=3, nodes_per_rod=100)):
+    for graphs in (True, False):
+        r, cs = rate(kw, 2048, cs_fused := False, graphs) if kw["rod_count"] * kw["nodes_per_rod"] > 256 else rate(kw, 2048, True)
+        print(f"{kw} graphs={graphs} fused={kw['rod_count'] * kw['nodes_per_rod'] <= 256}: {r:,.0f} RK2 steps/s")
+for graphs in (True, False, True, False):
+    r, _ = rate(dict(rod_count=64, nodes_per_rod=256, epsilon=0.08), 100, False, graphs)
+    print(f"64x256 graphs={graphs}: {r:,.1f} RK2 steps/s")
