@@ -40,9 +40,10 @@ for kw, steps in [(dict(rod_count=1, nodes_per_rod=100), 20000), (dict(rod_count
 # the paper's benchmark sizes (4 / 12 / 25 rods x 51 nodes), per-step kernels
 for kw in (dict(rod_count=4, nodes_per_rod=51), dict(rod_count=12, nodes_per_rod=51),
            dict(rod_count=25, nodes_per_rod=51), dict(rod_count=3, nodes_per_rod=100)):
+    fused = kw["rod_count"] * kw["nodes_per_rod"] <= 256  # fused path where eligible, else per-step kernels
     for graphs in (True, False):
-        r, cs = rate(kw, 2048, cs_fused := False, graphs) if kw["rod_count"] * kw["nodes_per_rod"] > 256 else rate(kw, 2048, True)
-        print(f"{kw} graphs={graphs} fused={kw['rod_count'] * kw['nodes_per_rod'] <= 256}: {r:,.0f} RK2 steps/s")
+        r, cs = rate(kw, 2048, fused, graphs)
+        print(f"{kw} graphs={graphs} fused={fused}: {r:,.0f} RK2 steps/s")
 for graphs in (True, False, True, False):
     r, _ = rate(dict(rod_count=64, nodes_per_rod=256, epsilon=0.08), 100, False, graphs)
     print(f"64x256 graphs={graphs}: {r:,.1f} RK2 steps/s")
