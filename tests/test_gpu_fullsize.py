@@ -1,6 +1,7 @@
 """Parity at BASELINE.json's full sizes through sampled rows and size-independent properties:
-MRS at N = 65,536 and 131,072 (configs[4]: 512 x 256) -- oracle rows, linearity in the loads,
-bitwise repeats, kernel-variant independence -- and one RK2 step of the 64 x 256 suspension
+MRS at N = 65,536, 131,072 (configs[4]: 512 x 256) and 1,048,576 (8x beyond it: 3.6 s per
+evaluation, 1.8 GB of split-source partials) -- oracle rows, linearity in the loads,
+bitwise repeats -- and one RK2 step of the 64 x 256 suspension
 (configs[2]) against the reference restatement."""
 import os
 
@@ -16,7 +17,7 @@ def _inputs(n, seed):
     return (rng.uniform(-0.5, 0.5, (n, 3)) for _ in range(3))
 
 
-@pytest.mark.parametrize("n", [65536, 131072])
+@pytest.mark.parametrize("n", [65536, 131072, 1048576])
 def test_mrs_full_size_rows_linearity_repeat(gpu, oracle, n):
     import torch
 
