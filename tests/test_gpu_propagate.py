@@ -268,3 +268,39 @@ def test_graph_replay_bitwise_equals_step_loop(gpu, oracle, kw, scheme, steps):
     assert oracle.position_metric(want, a) < 1e-10
     g.close()
     p.close()
+
+
+@pytest.mark.parametrize("kw", [dict(rod_count=1, nodes_per_rod=3), dict(rod_count=2, nodes_per_rod=3),
+                                dict(rod_count=5, nodes_per_rod=3), dict(rod_count=130, nodes_per_rod=3),
+                                dict(rod_count=1, nodes_per_rod=257), dict(rod_count=3, nodes_per_rod=86)])
+def test_edge_sizes_vs_oracle(gpu, oracle, kw):
+    """Ragged and extreme layouts: the shortest rods the reference accepts (3 nodes), one rod
+    just over the fused limit,
+    node counts that are not multiples of the warp tile (30 / 31 nodes) or of the MRS target
+    block (256): rhs and a short RK2 propagate against the oracle; fused and launched paths
+    (and the graph replay) agree bitwise where both apply."""
+    from oracle.pyoracle import Scenario as OS
+    from paper_2604_12083_b200.device import Context
+    from paper_2604_12083_b200.propagators import StepperConfig, propagate, rhs
+    from paper_2604_12083_b200.scenario import build_initial_state
+
+    kw = dict(kw, epsilon=0.08)
+    sc = scen(**kw)
+    x = build_initial_state(sc)
+    osc = OS.make(**kw)
+    v = rhs(x, 0.0, sc)
+    ou, ow = oracle.rhs(osc, x, 0.0)
+    scale = max(np.abs(ou).max(), np.abs(ow).max(), 1e-300)
+    assert max(np.abs(v.u - ou).max(), np.abs(v.omega - ow).max()) <= 1e-10 * scale
+    steps = 40
+    cfg = StepperConfig(0.0, 1, steps)
+    a_ctx, b_ctx = Context(0, sc), Context(0, sc)
+    b_ctx.lib.pswim_set_fused(b_ctx.handle, 0)
+    b_ctx.lib.pswim_set_graphs(b_ctx.handle, 0)
+    a = propagate(x, 0.0, steps * 1e-6, cfg, sc, ctx=a_ctx)
+    b = propagate(x, 0.0, steps * 1e-6, cfg, sc, ctx=b_ctx)
+    assert np.array_equal(a, b)
+    want = oracle.propagate(osc, x, 0.0, steps * 1e-6, 1, steps=steps)
+    assert oracle.position_metric(want, a) < 1e-10
+    a_ctx.close()
+    b_ctx.close()
