@@ -413,7 +413,26 @@ def time_steps_leg(args, world, rank, local, dev):
         t0 = time.perf_counter()
         res = pr.run_sliced_rank(plan, sc, fine_steps, coarse_steps, x0, local, transport=tr)
         wall = reduce_max(time.perf_counter() - t0, dev)
+        # the same fine propagation serially on one GPU (rank 0), for the speedup
+        serial = None
+        barrier()
+        if rank == 0:
+            from paper_2604_12083_b200.device import Context, dptr
+
+            sctx = Context(local, sc)
+            dx = torch.as_tensor(x0, device=dev)
+            dout = torch.empty_like(dx)
+            sctx.check(sctx.lib.pswim_propagate(sctx.handle, dptr(dx), 0.0, fine_steps * 1e-6, 1, fine_steps, 0.0,
+                                                dptr(dout)))
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            sctx.check(sctx.lib.pswim_propagate(sctx.handle, dptr(dx), 0.0, fine_steps * 1e-6, 1, fine_steps, 0.0,
+                                                dptr(dout)))
+            serial = world * (time.perf_counter() - t1)  # n intervals of serial fine
+            sctx.close()
+        barrier()
         leg = {"metric": "simulated RK2 time-steps/s", "value": world * fine_steps / wall, "unit": "steps/s",
+               "speedup_vs_serial_fine": (serial / wall) if serial else None,
                "config": {"workload": "pipelined Parareal, one slice per GPU, 64 x 256 suspension (BASELINE configs[3])",
                           "intervals": world, "fine_rk2_steps_per_interval": fine_steps,
                           "coarse_euler_steps_per_interval": coarse_steps, "iterations": res.report.iterations_used,

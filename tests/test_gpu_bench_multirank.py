@@ -36,6 +36,7 @@ def test_bench_multirank_gloo_wire(gpu, world):
     assert d["n_gpus"] == world and d["value"] > 0
     ts = d["time_steps"]
     assert "error" not in ts and ts["value"] > 0 and ts["config"]["intervals"] == world, ts
+    assert ts["speedup_vs_serial_fine"] > 0
     sp = ts["space_parallel"]
     assert "error" not in sp and sp["value"] > 0, sp
     assert "error" not in sp["fused_peer_allgather"], sp
