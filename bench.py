@@ -547,7 +547,7 @@ def flagellum_leg(args, local, dev):
     sc = make_scenario(ScenarioConfig(**kw))
     x0 = build_initial_state(sc)
     ctx = Context(local, sc)
-    cs = ctx.lib.pswim_set_fused(ctx.handle, 1)
+    cs = ctx.lib.pswim_set_fused(ctx.handle, 16)  # a lone system: 16-CTA clusters
     dx = torch.as_tensor(x0, device=dev)
     out = torch.empty_like(dx)
     L = ctx.lib

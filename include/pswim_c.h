@@ -182,8 +182,10 @@ int pswim_propagate(pswim_ctx* ctx, const double* d_in, double t0, double t1, in
 
 /* Small systems (N <= 256 nodes) propagate a whole interval in one fused cluster kernel
  * (state resident in shared memory, MRS partials exchanged through distributed shared
- * memory), bitwise identical to the per-step launched path.  Enabled by default; returns
- * the cluster size used for the context's scenario (0 = not eligible). */
+ * memory), bitwise identical to the per-step launched path.  enable: 0 off, 1 on (default:
+ * clusters of <= 8 CTAs), 2 / 4 / 8 / 16 on with that cluster-size cap (16: a lone small
+ * system on an otherwise idle GPU).  Returns the cluster size used for the context's
+ * scenario (0 = not eligible). */
 int pswim_set_fused(pswim_ctx* ctx, int enable);
 
 /* The fused small-system propagate (pswim_set_fused) with its in-kernel phase timer on:

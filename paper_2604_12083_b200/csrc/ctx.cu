@@ -220,9 +220,10 @@ int pswim_ctx::propagate_async(const double* d_in, double t0, double t1, int sch
         }
         return PSWIM_OK;
     }
-    if (fused_on && !timing_on && fused_cluster_size(rp) > 0) {
+    if (fused_on && !timing_on && fused_cluster_size(rp, fused_max_cs) > 0) {
         // the whole interval in one launch, bitwise identical to the loop below
-        const cudaError_t e = fused_propagate_launch(rp, d_out, steps, t0, dt, scheme, d_flags, stream);
+        const cudaError_t e = fused_propagate_launch(rp, d_out, steps, t0, dt, scheme, d_flags, stream, nullptr,
+                                                     fused_max_cs);
         if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("fused_propagate: ") + cudaGetErrorString(e));
         return PSWIM_OK;
     }
@@ -612,7 +613,7 @@ int pswim_propagate_host(pswim_ctx* ctx, const double* h_in, double t0, double t
 int pswim_fused_profile(pswim_ctx* ctx, const double* d_in, double t0, double t1, int scheme, int64_t spi,
                         double* d_out, uint64_t* h_cycles7) {
     if (!ctx || !h_cycles7) return PSWIM_EINVAL;
-    if (!ctx->has_scenario || fused_cluster_size(ctx->rp) == 0)
+    if (!ctx->has_scenario || fused_cluster_size(ctx->rp, ctx->fused_max_cs) == 0)
         return ctx->fail(PSWIM_EINVAL, "fused_profile: scenario not eligible for the fused path");
     int rc = ctx->use();
     if (rc) return rc;
@@ -626,7 +627,9 @@ int pswim_fused_profile(pswim_ctx* ctx, const double* d_in, double t0, double t1
     cudaError_t e = cudaMemsetAsync(prof, 0, sizeof(unsigned long long) * kFusedPhases, ctx->stream);
     if (e == cudaSuccess && d_in != d_out)
         e = cudaMemcpyAsync(d_out, d_in, bytes, cudaMemcpyDeviceToDevice, ctx->stream);
-    if (e == cudaSuccess) e = fused_propagate_launch(ctx->rp, d_out, steps, t0, dt, scheme, ctx->d_flags, ctx->stream, prof);
+    if (e == cudaSuccess)
+        e = fused_propagate_launch(ctx->rp, d_out, steps, t0, dt, scheme, ctx->d_flags, ctx->stream, prof,
+                                   ctx->fused_max_cs);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(h_cycles7, prof, sizeof(unsigned long long) * kFusedPhases, cudaMemcpyDeviceToHost,
                             ctx->stream);
@@ -653,7 +656,8 @@ int pswim_set_lj_mode(pswim_ctx* ctx, int mode) {
 int pswim_set_fused(pswim_ctx* ctx, int enable) {
     if (!ctx) return PSWIM_EINVAL;
     ctx->fused_on = enable != 0;
-    return ctx->has_scenario ? fused_cluster_size(ctx->rp) : 0;
+    ctx->fused_max_cs = (enable == 2 || enable == 4 || enable == 8 || enable == 16) ? enable : 0;
+    return ctx->has_scenario ? fused_cluster_size(ctx->rp, ctx->fused_max_cs) : 0;
 }
 
 int pswim_propagate_sharded(pswim_ctx* ctx, const pswim_transport* tr, const double* d_in, double t0, double t1,

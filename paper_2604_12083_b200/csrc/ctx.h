@@ -40,6 +40,7 @@ struct pswim_ctx {
     };
     bool timing_on = false;
     bool fused_on = true;  // whole-interval fused kernel for N <= 256 (fused.cu)
+    int fused_max_cs = 0;  // cluster-size cap (pswim_set_fused 2..16), 0 = default
     int lj_mode = 0;       // 0 auto (all-pairs below kLjCellsMinNodes), 1 all-pairs, 2 cell list
     pswim::LjWork lj_work;
     std::vector<TimedStage> open_stages, done_stages;

@@ -366,19 +366,23 @@ cudaError_t launch_cs(const FusedArgs& a, size_t smem, double* state, int64_t st
 }  // namespace
 
 // Returns the cluster size the fused path would use for this scenario (0 = not eligible).
-int fused_cluster_size(const RodParams& p) {
+int fused_cluster_size(const RodParams& p, int max_hint) {
     const int64_t n = p.rods * p.m;
     if (n > 256 || n < 2) return 0;
     const MrsPlan plan = mrs_plan(n, n);
-    static const int max_cs = [] {
+    static const int max_cs_env = [] {
         const char* e = std::getenv("PSWIM_FUSED_MAX_CLUSTER");
         const int v = e ? std::atoi(e) : 8;
         return (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) ? v : 8;
     }();
-    static const int min_tpc = [] {
+    static const int min_tpc_env = [] {
         const char* e = std::getenv("PSWIM_FUSED_MIN_TARGETS");
         return e ? std::max(1, std::atoi(e)) : 12;
     }();
+    // a per-context hint (pswim_set_fused 2..16) overrides the default: a lone small system
+    // runs fastest on 16 CTAs (>= 6 targets each); concurrent Parareal lanes keep <= 8
+    const int max_cs = max_hint >= 2 ? max_hint : max_cs_env;
+    const int min_tpc = max_hint >= 16 ? 6 : min_tpc_env;
     int cs = 1;
     while (cs < max_cs && (n + 2 * cs - 1) / (2 * cs) >= min_tpc) cs *= 2;  // >= min_tpc targets per CTA
     const int64_t tpc = (n + cs - 1) / cs;
@@ -400,8 +404,8 @@ void fused_preload() {
 }
 
 cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t steps, double t0, double dt, int scheme,
-                                   unsigned* flags, cudaStream_t st, unsigned long long* prof) {
-    const int cs = fused_cluster_size(p);
+                                   unsigned* flags, cudaStream_t st, unsigned long long* prof, int max_hint) {
+    const int cs = fused_cluster_size(p, max_hint);
     if (cs == 0) return cudaErrorInvalidValue;
     const int64_t n = p.rods * p.m;
     const MrsPlan plan = mrs_plan(n, n);

@@ -117,11 +117,13 @@ cudaError_t dfma_launch(double* sink, int blocks, int iters, cudaStream_t st);
 
 // ---- fused small-system propagator (fused.cu) ---------------------------------------------
 // Cluster size the fused path uses for this scenario (0 = not eligible: N > 256 or smem).
-int fused_cluster_size(const RodParams& p);
+// max_hint: 0 = default sizing (<= 8 CTAs, >= 12 targets each), 2..16 = cap
+int fused_cluster_size(const RodParams& p, int max_hint = 0);
 // prof: optional kFusedPhases device counters (in-kernel clock64 phase timer, fused.cu)
 constexpr int kFusedPhases = 7;
 cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t steps, double t0, double dt, int scheme,
-                                   unsigned* flags, cudaStream_t st, unsigned long long* prof = nullptr);
+                                   unsigned* flags, cudaStream_t st, unsigned long long* prof = nullptr,
+                                   int max_hint = 0);
 
 // ---- host scenario (scenario.cpp) -------------------------------------------------------
 int resolve_scenario(const pswim_scenario* sc, pswim_resolved* out, std::string* err);

@@ -304,3 +304,23 @@ def test_edge_sizes_vs_oracle(gpu, oracle, kw):
     assert oracle.position_metric(want, a) < 1e-10
     a_ctx.close()
     b_ctx.close()
+
+
+def test_fused_cluster_cap_bitwise(gpu):
+    """pswim_set_fused(ctx, 16): the flagellum on 16-CTA clusters, bitwise equal to the
+    default 8-CTA cluster and to the launched path (the cluster size only splits targets)."""
+    from paper_2604_12083_b200.device import Context
+    from paper_2604_12083_b200.propagators import StepperConfig, propagate
+    from paper_2604_12083_b200.scenario import build_initial_state
+
+    sc = scen(rod_count=1, nodes_per_rod=100)
+    x = build_initial_state(sc)
+    c16, c8, cl = Context(0, sc), Context(0, sc), Context(0, sc)
+    assert c16.lib.pswim_set_fused(c16.handle, 16) == 16
+    assert c8.lib.pswim_set_fused(c8.handle, 1) == 8
+    cl.lib.pswim_set_fused(cl.handle, 0)
+    cfg = StepperConfig(0.0, 1, 30)
+    outs = [propagate(x, 0.0, 3e-5, cfg, sc, ctx=c) for c in (c16, c8, cl)]
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    for c in (c16, c8, cl):
+        c.close()
