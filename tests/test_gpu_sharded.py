@@ -11,7 +11,12 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("world,kw", [(2, dict(rod_count=4, nodes_per_rod=100)),
                                       (3, dict(rod_count=9, nodes_per_rod=64, epsilon=0.08)),
-                                      (4, dict(rod_count=3, nodes_per_rod=200, epsilon=0.08))])
+                                      (4, dict(rod_count=3, nodes_per_rod=200, epsilon=0.08)),
+                                      # LJ through the cell list (N >= 2048) inside every rank's rhs
+                                      (2, dict(rod_count=40, nodes_per_rod=64, placement=1, lj_well_depth=0.01,
+                                               seed=5, epsilon=0.08)),
+                                      # 64 x 256: the MRS plan with 37 source chunks
+                                      (3, dict(rod_count=64, nodes_per_rod=256, epsilon=0.08))])
 def test_sharded_propagate_bitwise(gpu, world, kw):
     import torch
     from paper_2604_12083_b200.device import Context
