@@ -6,7 +6,9 @@ own streams; all arithmetic runs in libpswim.so's kernels.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
+import weakref
 from typing import Optional
 
 import numpy as np
@@ -29,6 +31,20 @@ def as_scenario_struct(sc) -> Optional[_lib.Scenario]:
     return sc.to_c()
 
 
+_LIVE: "weakref.WeakSet[Context]" = weakref.WeakSet()
+
+
+@atexit.register
+def _close_live_contexts() -> None:
+    # release every context while the CUDA runtime is still up (interpreter teardown would
+    # otherwise destroy them in an arbitrary order against torch's own CUDA state)
+    for ctx in list(_LIVE):
+        try:
+            ctx.close()
+        except Exception:
+            pass
+
+
 class Context:
     """One device stream with preallocated workspaces (pswim_create, include/pswim_c.h)."""
 
@@ -42,6 +58,7 @@ class Context:
         self.handle = h
         self.lib = L
         self._torch_stream = None
+        _LIVE.add(self)
 
     def close(self) -> None:
         if getattr(self, "handle", None):
