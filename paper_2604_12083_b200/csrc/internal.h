@@ -25,6 +25,7 @@ struct MrsPlan {
     int chunks = 0;         // source chunks (grid.y)
     size_t scratch_doubles = 0;
     size_t counters = 0;
+    int variant = 0;  // kernel variant forced by the plan (0 = mrs_targets_per_thread())
 };
 constexpr int kMrsThreads = 256;  // targets per block (one or two per thread)
 
