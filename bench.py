@@ -249,7 +249,7 @@ def run_ours(args) -> None:
     # --- e2e through the C-ABI host entry point, pinned host buffers ---
     hx, hf, hn = (torch.as_tensor(a).pin_memory() for a in (x, f, tq))
     hu = torch.empty((n, 3), dtype=torch.float64).pin_memory()
-    hw = torch.empty_like(hu)
+    hw = torch.empty((n, 3), dtype=torch.float64).pin_memory()  # (empty_like does not pin)
     P = C.POINTER(C.c_double)
 
     def hp(t):

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -438,6 +439,14 @@ void* pswim_stream(pswim_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
 int pswim_device(const pswim_ctx* ctx) { return ctx ? ctx->device : -1; }
 int pswim_sync(pswim_ctx* ctx) { return ctx ? ctx->sync() : PSWIM_EINVAL; }
 
+static bool direct_out_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PSWIM_DIRECT_OUT");  // dev knob: 0 = always copy back
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 static int check_kp(pswim_ctx* ctx, const pswim_kernel_params* kp) {
     // check_inputs, stokes.cpp:12-17
     if (!kp || kp->epsilon <= 0.0 || kp->mu <= 0.0) return ctx->fail(PSWIM_EINVAL, "stokes: epsilon and mu must be positive");
@@ -469,6 +478,7 @@ int pswim_mrs_velocities_host(pswim_ctx* ctx, const double* h_t, int64_t nt, con
     if (!ctx) return PSWIM_EINVAL;
     int rc = check_kp(ctx, kp);
     if (rc) return rc;
+    if (nt < 0 || ns < 0) return ctx->fail(PSWIM_EINVAL, "stokes: negative sizes");
     if ((rc = ctx->use())) return rc;
     const size_t t3 = 3 * static_cast<size_t>(nt), s3 = 3 * static_cast<size_t>(ns);
     if ((rc = ctx->ensure(&ctx->h_in, &ctx->cap_in, t3 > 0 ? t3 : 1))) return rc;
@@ -479,15 +489,31 @@ int pswim_mrs_velocities_host(pswim_ctx* ctx, const double* h_t, int64_t nt, con
     if ((rc = ctx->ensure(&ctx->h_o2, &ctx->cap_o2, t3 > 0 ? t3 : 1))) return rc;
     // targets = sources (the rhs call, propagators.cpp:87): one copy serves both
     const bool same = h_t == h_s && nt == ns;
+    // outputs in page-locked host memory are written by the kernel itself (mapped, over PCIe:
+    // no separate device -> host copies)
+    double *out_u = ctx->h_o1, *out_w = ctx->h_o2;
+    bool direct = false;
+    if (nt > 0 && ns > 0 && direct_out_enabled()) {
+        cudaPointerAttributes au{}, aw{};
+        if (cudaPointerGetAttributes(&au, h_u) == cudaSuccess && cudaPointerGetAttributes(&aw, h_w) == cudaSuccess &&
+            au.type == cudaMemoryTypeHost && aw.type == cudaMemoryTypeHost && au.devicePointer && aw.devicePointer) {
+            out_u = static_cast<double*>(au.devicePointer);
+            out_w = static_cast<double*>(aw.devicePointer);
+            direct = true;
+        }
+        cudaGetLastError();
+    }
     if (!same) CK(cudaMemcpyAsync(ctx->h_in, h_t, t3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_a, h_s, s3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_b, h_f, s3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_c, h_n, s3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    rc = pswim_mrs_velocities(ctx, same ? ctx->h_a : ctx->h_in, nt, ctx->h_a, ctx->h_b, ctx->h_c, ns, kp, ctx->h_o1,
-                              ctx->h_o2);
+    rc = pswim_mrs_velocities(ctx, same ? ctx->h_a : ctx->h_in, nt, ctx->h_a, ctx->h_b, ctx->h_c, ns, kp, out_u,
+                              out_w);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(h_u, ctx->h_o1, t3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(h_w, ctx->h_o2, t3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (!direct) {
+        CK(cudaMemcpyAsync(h_u, ctx->h_o1, t3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(h_w, ctx->h_o2, t3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    }
     return ctx->sync();
 }
 

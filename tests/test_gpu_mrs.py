@@ -199,3 +199,56 @@ def test_mrs_golden_vectors(gpu, golden):
     nd = golden["mrs12_nodes"]
     got = evaluate_velocities(nd, nd, LoadSet(golden["mrs12_f"], golden["mrs12_n"]), KernelParams(0.15, 2.3))
     assert rel_err(got, (golden["mrs12_dense_u"], golden["mrs12_dense_w"])) < 1e-12
+
+
+@pytest.mark.parametrize("n,nt", [(16384, None), (5000, 3001), (700, None), (300, 77)])
+def test_mrs_host_entry_pinned_and_pageable(gpu, oracle, n, nt):
+    """pswim_mrs_velocities_host (the e2e entry): outputs in page-locked memory are written by
+    the kernel itself (mapped host memory), pageable ones are copied back.  Bitwise equal to
+    the device-pointer entry on the same inputs, for pinned and pageable host buffers, over
+    repeated calls."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2604_12083_b200 import _lib
+    from paper_2604_12083_b200.device import Context, dptr
+
+    t, s, f, tq = rand_inputs(n, 900 + n, nt=nt)
+    ctx = Context(0)
+    L, kp, P = ctx.lib, _lib.KernelParams(0.1, 1.0, 0, 0), C.POINTER(C.c_double)
+    m = len(t)
+    d = [torch.as_tensor(a, device=gpu) for a in (t, s, f, tq)]
+    du, dw = torch.empty_like(d[0]), torch.empty_like(d[0])
+    ctx.after_torch()
+    ctx.check(L.pswim_mrs_velocities(ctx.handle, dptr(d[0]), m, dptr(d[1]), dptr(d[2]), dptr(d[3]), n, C.byref(kp),
+                                     dptr(du), dptr(dw)))
+    ctx.sync()
+    ref_u, ref_w = du.cpu().numpy(), dw.cpu().numpy()
+    want = oracle.evaluate_velocities(t[:64], s, f, tq, 0.1, 1.0)
+    assert rel_err((ref_u[:64], ref_w[:64]), want) < TOL
+
+    def hp(a):
+        return C.cast(a.data_ptr(), P) if isinstance(a, torch.Tensor) else a.ctypes.data_as(P)
+
+    same = nt is None
+    for pinned in (True, False):
+        if pinned:
+            hs, hf, hn = (torch.as_tensor(a).pin_memory() for a in (s, f, tq))
+            ht = hs if same else torch.as_tensor(t).pin_memory()
+            hu, hw = torch.zeros((m, 3), dtype=torch.float64).pin_memory(), torch.zeros((m, 3), dtype=torch.float64).pin_memory()
+        else:
+            hs, hf, hn = (np.ascontiguousarray(a) for a in (s, f, tq))
+            ht = hs if same else np.ascontiguousarray(t)
+            hu, hw = np.zeros((m, 3)), np.zeros((m, 3))
+        for _ in range(3):
+            ctx.check(L.pswim_mrs_velocities_host(ctx.handle, hp(ht), m, hp(hs), hp(hf), hp(hn), n, C.byref(kp), hp(hu),
+                                                  hp(hw)))
+            gu = hu.numpy() if pinned else hu
+            gw = hw.numpy() if pinned else hw
+            assert np.array_equal(gu, ref_u) and np.array_equal(gw, ref_w)
+            (hu.zero_() if pinned else hu.fill(0.0))
+            (hw.zero_() if pinned else hw.fill(0.0))
+        del hs, hf, hn, ht, hu, hw
+    torch.cuda.synchronize()
+    ctx.close()
