@@ -26,6 +26,7 @@ struct MrsPlan {
     size_t scratch_doubles = 0;
     size_t counters = 0;
     int variant = 0;  // kernel variant forced by the plan (0 = mrs_targets_per_thread())
+    int tail = 0;     // 0: equal chunks; c1 << 8 | m: chunks after the first c1 are 1/m size
 };
 constexpr int kMrsThreads = 256;  // targets per block (one or two per thread)
 
@@ -41,6 +42,13 @@ struct PeerOut {
     unsigned long long* flag[kMaxPeers];
 };
 MrsPlan mrs_plan(int64_t nt, int64_t ns);
+// Chunk c covers sources [bound(c), bound(c + 1)), bound(c) = unit(c) ns / unit(C).
+int mrs_chunk_unit(const MrsPlan& p, int c);
+int64_t mrs_chunk_bound(const MrsPlan& p, int c);
+constexpr int kMrsMaxChunks = 160;
+struct MrsBounds {  // kernel parameter: unit(0..C) of the plan, unit(C) again at [kMrsMaxChunks]
+    int b[kMrsMaxChunks + 1];
+};
 // All-pairs kernel variant (1: 1 target/thread; 2: 2 targets/thread; 3: 2 targets/thread at
 // 3 CTAs/SM -- the default); env PSWIM_MRS_TPT overrides.
 int mrs_targets_per_thread();
