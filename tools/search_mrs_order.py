@@ -1,0 +1,156 @@
+"""Local search over the accumulation order of mrs_pair2 (dev tool).
+
+The FP64 pipe cost of the MRS pair loop depends on how many DFMAs read three register pairs
+from the register file (tools/sass_cost.py).  Which operands are reuse-cache hits depends on
+the SASS order ptxas emits, which follows the source order of the independent accumulation
+statements only loosely.  This tool permutes those statements (and the operand order inside
+each fma, which is bitwise neutral), compiles mrs.cu for sm_100a, and keeps the order with the
+lowest modelled cost.  Results are bitwise unchanged by construction: every accumulator keeps
+the relative order of its own updates.
+
+    python tools/search_mrs_order.py [iterations] [workers]
+
+The block between `// <acc-order>` and `// </acc-order>` in csrc/kernels.cuh is rewritten
+in place with the best order found.
+"""
+import os
+import random
+import re
+import shutil
+import subprocess
+import sys
+import tempfile
+from concurrent.futures import ThreadPoolExecutor
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CSRC = os.path.join(ROOT, "paper_2604_12083_b200", "csrc")
+KCUH = os.path.join(CSRC, "kernels.cuh")
+PAT = "mrs_kernelILb1ELb0ELi3ELi2E"
+NVCC = ["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
+        "-lineinfo", "-fmad=false", "-cubin"]
+STMT = re.compile(r"(\w)\.(\w+) = fma\(([^,]+), ([^,]+), \1\.\2\)")
+
+
+def parse(block):
+    out = []
+    for s in block.split(";"):
+        s = s.strip()
+        if not s or s.startswith("//"):
+            continue
+        m = STMT.fullmatch(s)
+        assert m, s
+        out.append(list(m.groups()))  # target, field, m1, m2
+    return out
+
+
+def render(stmts):
+    lines, cur = [], []
+    for t, f, m1, m2 in stmts:
+        cur.append(f"{t}.{f} = fma({m1}, {m2}, {t}.{f});")
+        if len(cur) == 2:
+            lines.append("    " + " ".join(cur))
+            cur = []
+    if cur:
+        lines.append("    " + " ".join(cur))
+    return "\n".join(lines) + "\n"
+
+
+ORIG_SEQ = None
+
+
+def key_order(stmts):
+    # per accumulator: the multiplier pair of each update, in order (operand order ignored)
+    d = {}
+    for t, f, m1, m2 in stmts:
+        d.setdefault((t, f), []).append(frozenset((m1, m2)))
+    return d
+
+
+def evaluate(args):
+    stmts, work = args
+    src = open(os.path.join(work, "kernels.cuh.tmpl")).read().replace("@@BLOCK@@", render(stmts))
+    open(os.path.join(work, "kernels.cuh"), "w").write(src)
+    cub = os.path.join(work, "m.cubin")
+    r = subprocess.run(NVCC + ["-o", cub, os.path.join(work, "mrs.cu")], capture_output=True, text=True)
+    if r.returncode:
+        return None
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sass_cost.py"), cub, PAT], capture_output=True,
+                         text=True).stdout
+    m = re.search(r"modelled FP64-pipe cycles (\d+)", out)
+    ru = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-res-usage", cub], capture_output=True, text=True).stdout
+    rm = re.search(PAT + r".*\n\s*REG:(\d+) STACK:(\d+)", ru)
+    if not m or not rm or int(rm.group(2)) > 0 or int(rm.group(1)) > 168:
+        return None
+    return int(m.group(1))
+
+
+def main():
+    global ORIG_SEQ
+    iters = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+    workers = int(sys.argv[2]) if len(sys.argv) > 2 else (os.cpu_count() or 4)
+    text = open(KCUH).read()
+    i0 = text.index("// <acc-order>\n") + len("// <acc-order>\n")
+    i1 = text.index("    // </acc-order>")
+    stmts = parse(text[i0:i1])
+    ORIG_SEQ = key_order(stmts)
+    tmpl = text[:i0] + "@@BLOCK@@" + text[i1:]
+    dirs = []
+    for w in range(workers):
+        d = tempfile.mkdtemp(prefix=f"acc{w}_", dir="/tmp")
+        pkg = os.path.join(d, "pkg", "csrc")
+        os.makedirs(pkg)
+        os.makedirs(os.path.join(d, "include"))
+        for f in os.listdir(CSRC):
+            if f.endswith((".cu", ".cuh", ".h")):
+                shutil.copy(os.path.join(CSRC, f), pkg)
+        shutil.copy(os.path.join(ROOT, "include", "pswim_c.h"), os.path.join(d, "include"))
+        open(os.path.join(pkg, "kernels.cuh.tmpl"), "w").write(tmpl)
+        dirs.append(pkg)
+
+    def ok(s):
+        return key_order(s) == ORIG_SEQ and all(
+            [x for x in key_order(s)[k]] == ORIG_SEQ[k] for k in ORIG_SEQ)
+
+    def mutate(s):
+        s = [list(x) for x in s]
+        for _ in range(random.randint(1, 3)):
+            r = random.random()
+            if r < 0.3:  # operand order inside one fma
+                k = random.randrange(len(s))
+                s[k][2], s[k][3] = s[k][3], s[k][2]
+            elif r < 0.7:  # swap two adjacent statements
+                k = random.randrange(len(s) - 1)
+                s[k], s[k + 1] = s[k + 1], s[k]
+            else:  # move one statement
+                k = random.randrange(len(s))
+                x = s.pop(k)
+                s.insert(random.randrange(len(s) + 1), x)
+        return s
+
+    with ThreadPoolExecutor(workers) as ex:
+        best = stmts
+        best_c = evaluate((stmts, dirs[0]))
+        print(f"start: {best_c} cycles (bound {204 / best_c:.3f})", flush=True)
+        for it in range(iters):
+            cands = []
+            while len(cands) < workers:
+                c = mutate(best)
+                if ok(c):
+                    cands.append(c)
+            res = list(ex.map(evaluate, [(c, dirs[i]) for i, c in enumerate(cands)]))
+            for c, v in zip(cands, res):
+                if v is not None and v <= best_c:
+                    if v < best_c:
+                        print(f"iter {it}: {v} cycles (bound {204 / v:.3f})", flush=True)
+                    best, best_c = c, v
+    text = open(KCUH).read()
+    i0 = text.index("// <acc-order>\n") + len("// <acc-order>\n")
+    i1 = text.index("    // </acc-order>")
+    open(KCUH, "w").write(text[:i0] + render(best) + text[i1:])
+    print(f"best: {best_c} cycles (bound {204 / best_c:.3f}); written to {KCUH}")
+    for d in dirs:
+        shutil.rmtree(os.path.dirname(os.path.dirname(d)), ignore_errors=True)
+
+
+if __name__ == "__main__":
+    main()
