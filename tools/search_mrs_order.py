@@ -10,8 +10,9 @@ the relative order of its own updates.
 
     python tools/search_mrs_order.py [iterations] [workers]
 
-The block between `// <acc-order>` and `// </acc-order>` in csrc/kernels.cuh is rewritten
-in place with the best order found.
+The blocks between `// <acc-order>` / `// </acc-order>` (accumulations) and `// <pre-order>` /
+`// </pre-order>` (the per-pair values: line order within def-use dependencies, operand order
+of products) in csrc/kernels.cuh are rewritten in place with the best found.
 """
 import os
 import random
@@ -66,9 +67,61 @@ def key_order(stmts):
     return d
 
 
+# ---- the prefix block: `const double name = expr, ...;` lines, reordered within their
+# def-use dependencies, with the two multiplicands of `fma(x, y, z)` / `x * y` swappable
+IDENT = re.compile(r"[A-Za-z_]\w*(?:\.[xy])?")
+PROD = re.compile(r"fma\(([^,()]+), ([^,()]+),|(\b[\w.]+) \* ([\w.]+)")
+
+
+def parse_pre(block):
+    lines = [l.strip() for l in block.strip().splitlines() if l.strip() and not l.strip().startswith("//")]
+    items = []
+    for l in lines:
+        assert l.startswith("const double ") and l.endswith(";"), l
+        body = l[len("const double "):-1]
+        defs = [d.split("=")[0].strip() for d in re.split(r",\s*(?=\w+ = )", body)]
+        uses = set(IDENT.findall(body.split("=", 1)[1])) - set(defs)
+        items.append({"text": l, "defs": set(defs), "uses": uses})
+    return items
+
+
+def render_pre(items):
+    return "".join("    " + it["text"] + "\n" for it in items)
+
+
+def pre_ok(items):
+    defined = set()
+    alldefs = set().union(*(it["defs"] for it in items))
+    for it in items:
+        if (it["uses"] & alldefs) - defined:
+            return False
+        defined |= it["defs"]
+    return True
+
+
+def pre_mutate(items):
+    items = [dict(x) for x in items]
+    if random.random() < 0.5:
+        k = random.randrange(len(items) - 1)
+        items[k], items[k + 1] = items[k + 1], items[k]
+    else:
+        k = random.randrange(len(items))
+        t = items[k]["text"]
+        ms = list(PROD.finditer(t))
+        if ms:
+            m = random.choice(ms)
+            if m.group(1):
+                rep = f"fma({m.group(2)}, {m.group(1)},"
+            else:
+                rep = f"{m.group(4)} * {m.group(3)}"
+            items[k]["text"] = t[:m.start()] + rep + t[m.end():]
+    return items
+
+
 def evaluate(args):
-    stmts, work = args
+    (stmts, pre), work = args
     src = open(os.path.join(work, "kernels.cuh.tmpl")).read().replace("@@BLOCK@@", render(stmts))
+    src = src.replace("@@PRE@@", render_pre(pre))
     open(os.path.join(work, "kernels.cuh"), "w").write(src)
     cub = os.path.join(work, "m.cubin")
     r = subprocess.run(NVCC + ["-o", cub, os.path.join(work, "mrs.cu")], capture_output=True, text=True)
@@ -93,7 +146,10 @@ def main():
     i1 = text.index("    // </acc-order>")
     stmts = parse(text[i0:i1])
     ORIG_SEQ = key_order(stmts)
-    tmpl = text[:i0] + "@@BLOCK@@" + text[i1:]
+    p0 = text.index("\n", text.index("// <pre-order>")) + 1
+    p1 = text.index("    // </pre-order>")
+    pre = parse_pre(text[p0:p1])
+    tmpl = text[:p0] + "@@PRE@@" + text[p1:i0] + "@@BLOCK@@" + text[i1:]
     dirs = []
     for w in range(workers):
         d = tempfile.mkdtemp(prefix=f"acc{w}_", dir="/tmp")
@@ -128,15 +184,20 @@ def main():
         return s
 
     with ThreadPoolExecutor(workers) as ex:
-        best = stmts
-        best_c = evaluate((stmts, dirs[0]))
+        best = (stmts, pre)
+        best_c = evaluate((best, dirs[0]))
         print(f"start: {best_c} cycles (bound {204 / best_c:.3f})", flush=True)
         for it in range(iters):
             cands = []
             while len(cands) < workers:
-                c = mutate(best)
-                if ok(c):
-                    cands.append(c)
+                if random.random() < 0.5:
+                    c = (mutate(best[0]), best[1])
+                    if ok(c[0]):
+                        cands.append(c)
+                else:
+                    c = (best[0], pre_mutate(best[1]))
+                    if pre_ok(c[1]):
+                        cands.append(c)
             res = list(ex.map(evaluate, [(c, dirs[i]) for i, c in enumerate(cands)]))
             for c, v in zip(cands, res):
                 if v is not None and v <= best_c:
@@ -146,7 +207,9 @@ def main():
     text = open(KCUH).read()
     i0 = text.index("// <acc-order>\n") + len("// <acc-order>\n")
     i1 = text.index("    // </acc-order>")
-    open(KCUH, "w").write(text[:i0] + render(best) + text[i1:])
+    p0 = text.index("\n", text.index("// <pre-order>")) + 1
+    p1 = text.index("    // </pre-order>")
+    open(KCUH, "w").write(text[:p0] + render_pre(best[1]) + text[p1:i0] + render(best[0]) + text[i1:])
     print(f"best: {best_c} cycles (bound {204 / best_c:.3f}); written to {KCUH}")
     for d in dirs:
         shutil.rmtree(os.path.dirname(os.path.dirname(d)), ignore_errors=True)
