@@ -169,7 +169,7 @@ def main():
 
     def mutate(s):
         s = [list(x) for x in s]
-        for _ in range(random.randint(1, 3)):
+        for _ in range(random.randint(1, 5)):
             r = random.random()
             if r < 0.3:  # operand order inside one fma
                 k = random.randrange(len(s))
