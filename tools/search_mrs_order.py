@@ -8,7 +8,10 @@ each fma, which is bitwise neutral), compiles mrs.cu for sm_100a, and keeps the 
 lowest modelled cost.  Results are bitwise unchanged by construction: every accumulator keeps
 the relative order of its own updates.
 
-    python tools/search_mrs_order.py [iterations] [workers]
+    python tools/search_mrs_order.py [iterations] [workers] [variant]
+
+variant 3 (default): mrs_pair2, blocks `<acc-order>` / `<pre-order>`; variant 1: mrs_pair
+(one target per thread), blocks `<acc-order-1>` / `<pre-order-1>`.
 
 The blocks between `// <acc-order>` / `// </acc-order>` (accumulations) and `// <pre-order>` /
 `// </pre-order>` (the per-pair values: line order within def-use dependencies, operand order
@@ -26,7 +29,10 @@ from concurrent.futures import ThreadPoolExecutor
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CSRC = os.path.join(ROOT, "paper_2604_12083_b200", "csrc")
 KCUH = os.path.join(CSRC, "kernels.cuh")
-PAT = "mrs_kernelILb1ELb0ELi3ELi2E"
+VARIANT = sys.argv[3] if len(sys.argv) > 3 else "3"
+PAT = "mrs_kernelILb1ELb0ELi3ELi2E" if VARIANT == "3" else "mrs_kernelILb1ELb0ELi1ELi1E"
+SUF = "" if VARIANT == "3" else "-1"
+IDEAL = 204
 NVCC = ["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
         "-lineinfo", "-fmad=false", "-cubin"]
 STMT = re.compile(r"(\w)\.(\w+) = fma\(([^,]+), ([^,]+), \1\.\2\)")
@@ -142,12 +148,12 @@ def main():
     iters = int(sys.argv[1]) if len(sys.argv) > 1 else 40
     workers = int(sys.argv[2]) if len(sys.argv) > 2 else (os.cpu_count() or 4)
     text = open(KCUH).read()
-    i0 = text.index("// <acc-order>\n") + len("// <acc-order>\n")
-    i1 = text.index("    // </acc-order>")
+    i0 = text.index(f"// <acc-order{SUF}>\n") + len(f"// <acc-order{SUF}>\n")
+    i1 = text.index(f"    // </acc-order{SUF}>")
     stmts = parse(text[i0:i1])
     ORIG_SEQ = key_order(stmts)
-    p0 = text.index("\n", text.index("// <pre-order>")) + 1
-    p1 = text.index("    // </pre-order>")
+    p0 = text.index("\n", text.index(f"// <pre-order{SUF}>")) + 1
+    p1 = text.index(f"    // </pre-order{SUF}>")
     pre = parse_pre(text[p0:p1])
     tmpl = text[:p0] + "@@PRE@@" + text[p1:i0] + "@@BLOCK@@" + text[i1:]
     dirs = []
@@ -205,10 +211,10 @@ def main():
                         print(f"iter {it}: {v} cycles (bound {204 / v:.3f})", flush=True)
                     best, best_c = c, v
     text = open(KCUH).read()
-    i0 = text.index("// <acc-order>\n") + len("// <acc-order>\n")
-    i1 = text.index("    // </acc-order>")
-    p0 = text.index("\n", text.index("// <pre-order>")) + 1
-    p1 = text.index("    // </pre-order>")
+    i0 = text.index(f"// <acc-order{SUF}>\n") + len(f"// <acc-order{SUF}>\n")
+    i1 = text.index(f"    // </acc-order{SUF}>")
+    p0 = text.index("\n", text.index(f"// <pre-order{SUF}>")) + 1
+    p1 = text.index(f"    // </pre-order{SUF}>")
     open(KCUH, "w").write(text[:p0] + render_pre(best[1]) + text[p1:i0] + render(best[0]) + text[i1:])
     print(f"best: {best_c} cycles (bound {204 / best_c:.3f}); written to {KCUH}")
     for d in dirs:
