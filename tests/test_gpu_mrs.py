@@ -85,6 +85,13 @@ def test_mrs_known_answers(gpu, oracle):
     hd = h_functions(r, 0.37)
     ho = np.array([oracle.h_functions(x, 0.37) for x in r])
     assert np.max(np.abs(hd - ho) / np.abs(ho)) < 1e-14
+    # far field approaches the singular kernels (test_stokes.cpp:49-60), < 1e-3
+    eps = 0.2
+    r = np.array([1e2, 1e3]) * eps
+    hf = h_functions(r, eps)
+    sing = np.stack([1 / (8 * np.pi * r), 1 / (8 * np.pi * r**3), 1 / (8 * np.pi * r**3), -1 / (16 * np.pi * r**3),
+                     3 / (16 * np.pi * r**5)], axis=1)
+    assert np.max(np.abs(hf - sing) / np.abs(sing)) < 1e-3
 
 
 def test_mrs_dense_oracle_n12(gpu, oracle):
