@@ -448,9 +448,65 @@ def time_steps_leg(args, world, rank, local, dev):
                 leg["hybrid_space_time"] = hybrid_leg(args, sc, x0, local, dev, world, members=2)
             except Exception as e:
                 leg["hybrid_space_time"] = {"error": f"{type(e).__name__}: {e}"}
+        if not args.no_large:
+            try:
+                leg["large_suspension"] = large_leg(args, local, dev, tr, world, rank)
+            except Exception as e:
+                leg["large_suspension"] = {"error": f"{type(e).__name__}: {e}"}
     finally:
         _lib_destroy(tr)
     return leg
+
+
+def large_leg(args, local, dev, tr, world, rank):
+    """BASELINE configs[4]: the 512 x 256 suspension (N = 131,072), pipelined Parareal with one
+    slice per GPU, swept over the iteration count l.  Simulated RK2 steps/s, the speedup over
+    the same fine propagation serially on one GPU, and the Parareal defect eta_tilde per l."""
+    import torch
+
+    from paper_2604_12083_b200 import parareal as pr
+    from paper_2604_12083_b200.device import Context, dptr
+    from paper_2604_12083_b200.scenario import ScenarioConfig, build_initial_state, make_scenario
+
+    rods = int(os.environ.get("PSWIM_BENCH_LARGE_RODS", "512"))  # (tests shrink it)
+    sc = make_scenario(ScenarioConfig(rod_count=rods, nodes_per_rod=256, epsilon=0.08, fine_dt=1e-6))
+    x0 = build_initial_state(sc)
+    fine, coarse = args.large_fine_steps, 1
+    # serial fine reference time: one interval on rank 0 (x world intervals)
+    serial = None
+    barrier()
+    if rank == 0:
+        sctx = Context(local, sc)
+        dx = torch.as_tensor(x0, device=dev)
+        dout = torch.empty_like(dx)
+        sctx.check(sctx.lib.pswim_propagate(sctx.handle, dptr(dx), 0.0, 1e-6, 1, 1, 0.0, dptr(dout)))  # warm-up
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        sctx.check(sctx.lib.pswim_propagate(sctx.handle, dptr(dx), 0.0, fine * 1e-6, 1, fine, 0.0, dptr(dout)))
+        torch.cuda.synchronize()
+        serial = world * (time.perf_counter() - t1)
+        sctx.close()
+    barrier()
+    warm = pr.ParallelPlan(t0=0.0, horizon=world * 1e-6, intervals=world, workers=world, max_iterations=1,
+                           tolerance=1e-300, mode=pr.PIPELINED)
+    pr.run_sliced_rank(warm, sc, 1, coarse, x0, local, transport=tr)  # contexts, kernels, plans
+    sweep = []
+    for l in range(1, min(world, args.large_max_iters) + 1):
+        plan = pr.ParallelPlan(t0=0.0, horizon=world * fine * 1e-6, intervals=world, workers=world,
+                               max_iterations=l, tolerance=1e-300, mode=pr.PIPELINED)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = pr.run_sliced_rank(plan, sc, fine, coarse, x0, local, transport=tr)
+        wall = reduce_max(time.perf_counter() - t0, dev)
+        sweep.append({"iterations": res.report.iterations_used, "value": world * fine / wall, "unit": "steps/s",
+                      "wall_s": wall, "speedup_vs_serial_fine": (serial / wall) if serial else None,
+                      "eta_tilde": res.report.eta_tilde})
+    return {"metric": "simulated RK2 time-steps/s", "unit": "steps/s",
+            "config": {"workload": f"pipelined Parareal, one slice per GPU, {rods} x 256 suspension (BASELINE configs[4])",
+                       "points": rods * 256, "intervals": world, "fine_rk2_steps_per_interval": fine,
+                       "coarse_euler_steps_per_interval": coarse},
+            "serial_fine_s": serial, "iteration_sweep": sweep}
 
 
 def hybrid_leg(args, sc, x0, local, dev, world, members):
@@ -684,6 +740,9 @@ def main():
     ap.add_argument("--parareal-iters", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (profiling runs)")
     ap.add_argument("--no-steps", action="store_true", help="skip the time-step leg")
+    ap.add_argument("--no-large", action="store_true", help="skip the N > 1 large-suspension sweep (configs[4])")
+    ap.add_argument("--large-fine-steps", type=int, default=4, help="RK2 steps per interval, large sweep")
+    ap.add_argument("--large-max-iters", type=int, default=3, help="largest Parareal iteration count swept")
     ap.add_argument("--wire", default="nccl", choices=["nccl", "gloo"],
                     help="N>1 transport; gloo = test mode (ranks may share one GPU, staged host transports)")
     args = ap.parse_args()

@@ -29,7 +29,8 @@ def test_bench_multirank_gloo_wire(gpu, world):
            "--master-addr", "127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "bench.py"),
            "--gpus", str(world), "--steps", "3", "--warmup", "3", "--wire", "gloo", "--fine-steps", "4",
            "--no-cpu"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    env = dict(os.environ, PSWIM_BENCH_LARGE_RODS="4")  # the configs[4] sweep code path, shrunk
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
     d = json.loads(lines[-1])
@@ -40,6 +41,9 @@ def test_bench_multirank_gloo_wire(gpu, world):
     sp = ts["space_parallel"]
     assert "error" not in sp and sp["value"] > 0, sp
     assert "error" not in sp["fused_peer_allgather"], sp
+    lg = ts["large_suspension"]
+    assert "error" not in lg and len(lg["iteration_sweep"]) == min(world, 3), lg
+    assert all(x["value"] > 0 and x["iterations"] == i + 1 for i, x in enumerate(lg["iteration_sweep"]))
     if world >= 4:
         hy = ts["hybrid_space_time"]
         assert "error" not in hy and hy["value"] > 0 and hy["config"]["iterations"] == 1, hy
