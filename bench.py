@@ -741,7 +741,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (profiling runs)")
     ap.add_argument("--no-steps", action="store_true", help="skip the time-step leg")
     ap.add_argument("--no-large", action="store_true", help="skip the N > 1 large-suspension sweep (configs[4])")
-    ap.add_argument("--large-fine-steps", type=int, default=4, help="RK2 steps per interval, large sweep")
+    ap.add_argument("--large-fine-steps", type=int, default=8, help="RK2 steps per interval, large sweep")
     ap.add_argument("--large-max-iters", type=int, default=3, help="largest Parareal iteration count swept")
     ap.add_argument("--wire", default="nccl", choices=["nccl", "gloo"],
                     help="N>1 transport; gloo = test mode (ranks may share one GPU, staged host transports)")
