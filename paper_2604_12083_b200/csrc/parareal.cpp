@@ -897,9 +897,14 @@ int rank_run(const pswim_plan& plan, SliceBackend& be, const pswim_transport& tr
     } while (0)
 
     auto launch_fine = [&](int k) -> int {
-        // F(X[k][n-1]) for iteration k+1, on the fine queue, after the input arrived
+        // F(X[k][n-1]) for iteration k+1, on the fine queue, after the input arrived and after
+        // this rank's own coarse / corrector on the same input produced X[k][n]: the coarse
+        // chain through the ranks is the sequential critical path, and sharing the GPU with
+        // its own fine solve slows each link (measured 4.65 -> 6.10 ms per coarse interval at
+        // 64 x 256, tools/probe_contention.py), while F only starts T_G later.
         if (k + 1 > Kn) return PSWIM_OK;
         if (has_prev) RK(be.wait(1, tag(k, kTagIn)));
+        RK(be.wait(1, tag(k, kTagX)));
         RK(be.fine(IN + k, t_lo, t_hi, FB + k + 1));
         return be.mark(1, tag(k + 1, kTagFine));
     };
