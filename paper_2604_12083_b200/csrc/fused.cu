@@ -222,7 +222,7 @@ __device__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t*
     double* lpart = sm + a.off_part;  // [chunks][tpc][6]
     for (int w = tid; w < nloc * a.chunks; w += bs) {
         const int c = w / nloc, il = w % nloc, i = i0 + il;
-        const int j0 = (int)((int64_t)c * N / a.chunks), j1 = (int)((int64_t)(c + 1) * N / a.chunks);
+        const int j0 = c * N / a.chunks, j1 = (c + 1) * N / a.chunks;  // (N <= 256: no overflow)
         const double tx = pos[3 * i] - ox, ty = pos[3 * i + 1] - oy, tz = pos[3 * i + 2] - oz;
         MrsAcc acc;
         acc.zero();
