@@ -11,7 +11,8 @@ the relative order of its own updates.
     python tools/search_mrs_order.py [iterations] [workers] [variant]
 
 variant 3 (default): mrs_pair2, blocks `<acc-order>` / `<pre-order>`; variant 1: mrs_pair
-(one target per thread), blocks `<acc-order-1>` / `<pre-order-1>`.
+(one target per thread), blocks `<acc-order-1>` / `<pre-order-1>`; variant 4: mrs_pair4 (four
+targets per thread), blocks `<acc-order-4>` / `<pre-order-4>`.
 
 The blocks between `// <acc-order>` / `// </acc-order>` (accumulations) and `// <pre-order>` /
 `// </pre-order>` (the per-pair values: line order within def-use dependencies, operand order
@@ -30,9 +31,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CSRC = os.path.join(ROOT, "paper_2604_12083_b200", "csrc")
 KCUH = os.path.join(CSRC, "kernels.cuh")
 VARIANT = sys.argv[3] if len(sys.argv) > 3 else "3"
-PAT = "mrs_kernelILb1ELb0ELi3ELi2E" if VARIANT == "3" else "mrs_kernelILb1ELb0ELi1ELi1E"
-SUF = "" if VARIANT == "3" else "-1"
-IDEAL = 204
+PAT = {"3": "mrs_kernelILb1ELb0ELi3ELi2E", "1": "mrs_kernelILb1ELb0ELi1ELi1E",
+       "4": "mrs_kernelILb1ELb0ELi4ELi4E"}[VARIANT]
+SUF = {"3": "", "1": "-1", "4": "-4"}[VARIANT]
+IDEAL = 408 if VARIANT == "4" else 204  # 2 cycles per FP64 instruction of the loop body
 NVCC = ["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
         "-lineinfo", "-fmad=false", "-cubin"]
 STMT = re.compile(r"(\w)\.(\w+) = fma\(([^,]+), ([^,]+), \1\.\2\)")
@@ -138,7 +140,7 @@ def evaluate(args):
     m = re.search(r"modelled FP64-pipe cycles (\d+)", out)
     ru = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-res-usage", cub], capture_output=True, text=True).stdout
     rm = re.search(PAT + r".*\n\s*REG:(\d+) STACK:(\d+)", ru)
-    if not m or not rm or int(rm.group(2)) > 0 or int(rm.group(1)) > 168:
+    if not m or not rm or int(rm.group(2)) > 0 or int(rm.group(1)) > (255 if VARIANT == "4" else 168):
         return None
     return int(m.group(1))
 
@@ -192,7 +194,7 @@ def main():
     with ThreadPoolExecutor(workers) as ex:
         best = (stmts, pre)
         best_c = evaluate((best, dirs[0]))
-        print(f"start: {best_c} cycles (bound {204 / best_c:.3f})", flush=True)
+        print(f"start: {best_c} cycles (bound {IDEAL / best_c:.3f})", flush=True)
         for it in range(iters):
             cands = []
             while len(cands) < workers:
@@ -208,7 +210,7 @@ def main():
             for c, v in zip(cands, res):
                 if v is not None and v <= best_c:
                     if v < best_c:
-                        print(f"iter {it}: {v} cycles (bound {204 / v:.3f})", flush=True)
+                        print(f"iter {it}: {v} cycles (bound {IDEAL / v:.3f})", flush=True)
                     best, best_c = c, v
     text = open(KCUH).read()
     i0 = text.index(f"// <acc-order{SUF}>\n") + len(f"// <acc-order{SUF}>\n")
@@ -216,7 +218,7 @@ def main():
     p0 = text.index("\n", text.index(f"// <pre-order{SUF}>")) + 1
     p1 = text.index(f"    // </pre-order{SUF}>")
     open(KCUH, "w").write(text[:p0] + render_pre(best[1]) + text[p1:i0] + render(best[0]) + text[i1:])
-    print(f"best: {best_c} cycles (bound {204 / best_c:.3f}); written to {KCUH}")
+    print(f"best: {best_c} cycles (bound {IDEAL / best_c:.3f}); written to {KCUH}")
     for d in dirs:
         shutil.rmtree(os.path.dirname(os.path.dirname(d)), ignore_errors=True)
 
