@@ -259,3 +259,31 @@ def test_mrs_host_entry_pinned_and_pageable(gpu, oracle, n, nt):
         del hs, hf, hn, ht, hu, hw
     torch.cuda.synchronize()
     ctx.close()
+
+
+def test_mrs_kernel_variants_bitwise(gpu):
+    """The four all-pairs kernel variants (PSWIM_MRS_TPT = 1..4: one, two (2 and 3 CTAs/SM)
+    and four targets per thread) run the same per-target operation sequence on the same
+    chunk plan, so their outputs are bitwise identical (the variant is read once per
+    process, hence one subprocess each)."""
+    import subprocess
+    import sys
+
+    code = ("import hashlib, numpy as np, torch\n"
+            "from paper_2604_12083_b200.stokes import KernelParams, LoadSet, evaluate_velocities\n"
+            "rng = np.random.default_rng(5)\n"
+            "for n in (300, 2053, 16384):\n"
+            "    d = [torch.as_tensor(rng.uniform(-0.5, 0.5, (n, 3)), device='cuda') for _ in range(3)]\n"
+            "    r = evaluate_velocities(d[0], d[0], LoadSet(d[1], d[2]), KernelParams(0.1, 1.0))\n"
+            "    print(hashlib.sha1(r.u.cpu().numpy().tobytes() + r.omega.cpu().numpy().tobytes()).hexdigest())\n")
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for v in ("1", "2", "3", "4"):
+        env = dict(os.environ, PSWIM_MRS_TPT=v)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=root,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.split())
+    assert all(o == outs[0] for o in outs) and len(outs[0]) == 3, outs
