@@ -191,6 +191,21 @@ def main():
                 s.insert(random.randrange(len(s) + 1), x)
         return s
 
+    if os.environ.get("SEARCH_RESTART"):  # start from a random valid accumulation order
+        random.seed(int(os.environ["SEARCH_RESTART"]))
+        sh = [list(x) for x in stmts]
+        random.shuffle(sh)
+        # restore each accumulator's own update order (positions kept, contents reassigned)
+        pos = {}
+        for i, (t, f, _, _) in enumerate(sh):
+            pos.setdefault((t, f), []).append(i)
+        orig = {}
+        for x in stmts:
+            orig.setdefault((x[0], x[1]), []).append(list(x))
+        for key, idx in pos.items():
+            for i, x in zip(idx, orig[key]):
+                sh[i] = x
+        stmts = sh
     with ThreadPoolExecutor(workers) as ex:
         best = (stmts, pre)
         best_c = evaluate((best, dirs[0]))
