@@ -125,8 +125,9 @@ int pswim_mrs_velocities(pswim_ctx* ctx, const double* d_targets, int64_t n_targ
 
 /* Same operator through host buffers (H2D copies, kernel, D2H copies, sync, error check).
  * Page-locked (cudaHostAlloc / cudaHostRegister) output buffers are written by the kernel
- * directly (mapped host memory, no D2H copies); pageable ones are copied back.  Synchronous:
- * the outputs are complete when the call returns. */
+ * directly (mapped host memory, no D2H copies) and page-locked inputs are read by an upload
+ * kernel; pageable buffers take DMA copies.  Synchronous: the outputs are complete when the
+ * call returns. */
 int pswim_mrs_velocities_host(pswim_ctx* ctx, const double* h_targets, int64_t n_targets,
                               const double* h_sources, const double* h_f, const double* h_n,
                               int64_t n_sources, const pswim_kernel_params* kp, double* h_u,

@@ -447,6 +447,14 @@ static bool direct_out_enabled() {
     return on;
 }
 
+static bool upload_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PSWIM_SM_UPLOAD");  // dev knob: 0 = always DMA copies
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 static int check_kp(pswim_ctx* ctx, const pswim_kernel_params* kp) {
     // check_inputs, stokes.cpp:12-17
     if (!kp || kp->epsilon <= 0.0 || kp->mu <= 0.0) return ctx->fail(PSWIM_EINVAL, "stokes: epsilon and mu must be positive");
@@ -503,10 +511,36 @@ int pswim_mrs_velocities_host(pswim_ctx* ctx, const double* h_t, int64_t nt, con
         }
         cudaGetLastError();
     }
-    if (!same) CK(cudaMemcpyAsync(ctx->h_in, h_t, t3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->h_a, h_s, s3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->h_b, h_f, s3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->h_c, h_n, s3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    // inputs: page-locked (mapped) arrays are pulled by an SM upload kernel (many requests in
+    // flight), pageable ones by DMA copies
+    const double* dev_in[4] = {nullptr, nullptr, nullptr, nullptr};
+    bool mapped_in = ns > 0 && upload_enabled();
+    const double* hin[4] = {same ? nullptr : h_t, h_s, h_f, h_n};
+    for (int k = 0; k < 4 && mapped_in; ++k) {
+        if (!hin[k]) continue;
+        cudaPointerAttributes a{};
+        mapped_in = cudaPointerGetAttributes(&a, hin[k]) == cudaSuccess && a.type == cudaMemoryTypeHost &&
+                    a.devicePointer;
+        dev_in[k] = mapped_in ? static_cast<const double*>(a.devicePointer) : nullptr;
+    }
+    cudaGetLastError();
+    if (mapped_in) {
+        if (!same) {
+            const double* s1[3] = {dev_in[0], nullptr, nullptr};
+            double* d1[3] = {ctx->h_in, nullptr, nullptr};
+            const int64_t n1[3] = {(int64_t)t3, 0, 0};
+            CK(upload_launch(s1, d1, n1, ctx->stream));
+        }
+        const double* s3v[3] = {dev_in[1], dev_in[2], dev_in[3]};
+        double* d3v[3] = {ctx->h_a, ctx->h_b, ctx->h_c};
+        const int64_t n3[3] = {(int64_t)s3, (int64_t)s3, (int64_t)s3};
+        CK(upload_launch(s3v, d3v, n3, ctx->stream));
+    } else {
+        if (!same) CK(cudaMemcpyAsync(ctx->h_in, h_t, t3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->h_a, h_s, s3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->h_b, h_f, s3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->h_c, h_n, s3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    }
     rc = pswim_mrs_velocities(ctx, same ? ctx->h_a : ctx->h_in, nt, ctx->h_a, ctx->h_b, ctx->h_c, ns, kp, out_u,
                               out_w);
     if (rc) return rc;

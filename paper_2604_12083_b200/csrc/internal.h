@@ -79,6 +79,9 @@ cudaError_t peer_wait_launch(const unsigned long long* flag, unsigned long long 
 cudaError_t unshard_launch(const double* gathered, int64_t shard_targets, int64_t nt, double* u, double* w,
                            cudaStream_t st);
 cudaError_t h_functions_launch(const double* r, int64_t count, double eps, double* h5, cudaStream_t st);
+// Copies up to three mapped page-locked host arrays (src[k] device-accessible, nullptr = skip)
+// into device memory with SM loads (pswim_mrs_velocities_host).
+cudaError_t upload_launch(const double* const src[3], double* const dst[3], const int64_t n[3], cudaStream_t st);
 
 // ---- rod / propagator kernels (rod.cu) --------------------------------------------------
 struct RodParams {
