@@ -211,9 +211,10 @@ def test_mrs_golden_vectors(gpu, golden):
 @pytest.mark.parametrize("n,nt", [(16384, None), (5000, 3001), (700, None), (300, 77)])
 def test_mrs_host_entry_pinned_and_pageable(gpu, oracle, n, nt):
     """pswim_mrs_velocities_host (the e2e entry): outputs in page-locked memory are written by
-    the kernel itself (mapped host memory), pageable ones are copied back.  Bitwise equal to
-    the device-pointer entry on the same inputs, for pinned and pageable host buffers, over
-    repeated calls."""
+    the kernel itself (mapped host memory), pageable ones are copied back; page-locked inputs
+    go through the SM upload kernel (16-B and, for an 8-B-aligned view, scalar loads).
+    Bitwise equal to the device-pointer entry on the same inputs, for pinned (aligned and
+    not) and pageable host buffers, over repeated calls."""
     import ctypes as C
 
     import torch
@@ -239,10 +240,20 @@ def test_mrs_host_entry_pinned_and_pageable(gpu, oracle, n, nt):
         return C.cast(a.data_ptr(), P) if isinstance(a, torch.Tensor) else a.ctypes.data_as(P)
 
     same = nt is None
-    for pinned in (True, False):
+
+    def pinned_view(a, off):
+        # page-locked copy of `a` starting `off` doubles into its allocation (off = 1: 8-B
+        # aligned only, the upload kernel's scalar path)
+        buf = torch.empty(a.size + off, dtype=torch.float64).pin_memory()
+        v = buf[off:].view(a.shape)
+        v.copy_(torch.as_tensor(a))
+        return v
+
+    for pinned in (True, "unaligned", False):
         if pinned:
-            hs, hf, hn = (torch.as_tensor(a).pin_memory() for a in (s, f, tq))
-            ht = hs if same else torch.as_tensor(t).pin_memory()
+            off = 1 if pinned == "unaligned" else 0
+            hs, hf, hn = (pinned_view(a, off) for a in (s, f, tq))
+            ht = hs if same else pinned_view(t, off)
             hu, hw = torch.zeros((m, 3), dtype=torch.float64).pin_memory(), torch.zeros((m, 3), dtype=torch.float64).pin_memory()
         else:
             hs, hf, hn = (np.ascontiguousarray(a) for a in (s, f, tq))
