@@ -243,7 +243,7 @@ __device__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t*
     for (int w = tid; w < nloc * 6; w += bs) {
         const int il = w / 6, q = w - 6 * il;
         double sum = lpart[w];
-#pragma unroll 4
+#pragma unroll 8
         for (int c = 1; c < a.chunks; ++c) sum += lpart[(c * tpc + il) * 6 + q];
         const int i = i0 + il;
         if constexpr (CS > 1) {
