@@ -15,3 +15,10 @@ ncu --set full --clock-control none --import-source on -k regex:"fused_kernel" -
     python tools/probe_steps.py > gpurun_out/ncu_fused.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/lj_launches.csv \
     python tools/probe_lj.py > gpurun_out/ncu_lj.log 2>&1
+# round-end extras (this round): e2e breakdown, per-CTA MRS timeline (needs
+# `python tools/probe_mrs_trace.py build` here first), sanitizers
+python tools/probe_e2e.py 16384 4096 > gpurun_out/e2e.txt 2>&1
+[ -f tools/libpswim_trace.so ] && python tools/probe_mrs_trace.py 16384 > gpurun_out/trace.txt 2>&1
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_smoke.py > gpurun_out/san_$tool.txt 2>&1
+done
