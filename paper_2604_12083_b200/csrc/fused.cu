@@ -36,6 +36,7 @@ struct FusedArgs {
     int n;        // total nodes
     int rods, m;  // layout
     int chunks;   // MRS source chunks (== mrs_plan(n, n).chunks)
+    unsigned m_magic;  // __umulhi(g, m_magic) == g / m for g, m < 2^16 (no division on the chains)
     int lj_on;
     double max_disp;
     // shared-memory offsets (doubles)
@@ -99,7 +100,7 @@ __device__ const double* fused_front(const FusedArgs& a, double* sm, const doubl
             if (valid && vadv) fl |= advance_node(src + 12 * g, vadv + 6 * g, vadv + 6 * g + 3, h, a.max_disp, tile + 12 * lane);
             __syncwarp();
             pc.mark(1);
-            const int rod = valid ? g / m : 0, k = valid ? g - rod * m : 0;
+            const int rod = valid ? (int)__umulhi((unsigned)g, a.m_magic) : 0, k = valid ? g - rod * m : 0;
             const double* xs = vadv ? tile + 12 * (rod * m - base) : src + 12 * rod * m;  // rod's node 0
             double seg[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             if (valid && lane < 31 && k + 1 < m)
@@ -220,8 +221,9 @@ __device__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t*
     const int tpc = (N + CS - 1) / CS;
     const int i0 = rank * tpc, i1 = min(N, i0 + tpc), nloc = max(0, i1 - i0);
     double* lpart = sm + a.off_part;  // [chunks][tpc][6]
+    const unsigned nloc_magic = nloc > 0 ? 0xFFFFFFFFu / (unsigned)nloc + 1u : 0u;  // w / nloc, w < 2^16
     for (int w = tid; w < nloc * a.chunks; w += bs) {
-        const int c = w / nloc, il = w % nloc, i = i0 + il;
+        const int c = (int)__umulhi((unsigned)w, nloc_magic), il = w - c * nloc, i = i0 + il;
         const int j0 = c * N / a.chunks, j1 = (c + 1) * N / a.chunks;  // (N <= 256: no overflow)
         const double tx = pos[3 * i] - ox, ty = pos[3 * i + 1] - oy, tz = pos[3 * i + 2] - oz;
         MrsAcc acc;
@@ -417,6 +419,7 @@ cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t st
     a.rods = (int)p.rods;
     a.m = (int)p.m;
     a.chunks = plan.chunks;
+    a.m_magic = 0xFFFFFFFFu / (unsigned)p.m + 1u;
     a.lj_on = (p.rods >= 2 && p.lj_well > 0.0) ? 1 : 0;  // propagators.cpp:70
     a.max_disp = 10.0 * p.ds;
     a.prof = prof;
