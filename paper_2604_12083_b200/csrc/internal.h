@@ -48,6 +48,8 @@ int64_t mrs_chunk_bound(const MrsPlan& p, int c);
 constexpr int kMrsMaxChunks = 160;
 struct MrsBounds {  // kernel parameter: unit(0..C) of the plan, unit(C) again at [kMrsMaxChunks]
     int b[kMrsMaxChunks + 1];
+    int main_chunks;  // c1: chunks before the tail split (C without one)
+    int tbs;          // target blocks of the plan (the second counter row)
 };
 // All-pairs kernel variant (1: 1 target/thread; 2: 2 targets/thread; 3: 2 targets/thread at
 // 3 CTAs/SM -- the default); env PSWIM_MRS_TPT overrides.
