@@ -140,7 +140,7 @@ int pswim_ctx::lj(const double* state, double* out) {
 int pswim_ctx::rhs(const double* state, double t, const double* ef, const double* en, double* u, double* w,
                    const double* tdev) {
     if (!has_scenario) return fail(PSWIM_EINVAL, "rhs: context has no scenario");
-    if (sc.wall_mode == 1) return fail(PSWIM_EUNSUPPORTED_WALL, "stokes: image_wall correction is not implemented; use free_space");
+    if (sc.wall_mode == 1) return fail(PSWIM_EUNSUPPORTED_WALL, kWallMsg);
     stage_begin(0);
     const bool lj = rp.rods >= 2 && rp.lj_well > 0.0;  // propagators.cpp:70
     if (lj) {
@@ -200,6 +200,8 @@ int pswim_ctx::resolve_steps(double t0, double t1, int64_t steps_per_interval, d
 int pswim_ctx::propagate_async(const double* d_in, double t0, double t1, int scheme, int64_t spi, double dtc,
                                double* d_out, const pswim_transport* space) {
     if (!has_scenario) return fail(PSWIM_EINVAL, "propagate: context has no scenario");
+    // checked here, not only in rhs: the fused, graph and sharded paths never reach rhs()
+    if (sc.wall_mode == 1) return fail(PSWIM_EUNSUPPORTED_WALL, kWallMsg);
     const size_t bytes = sizeof(double) * 12 * static_cast<size_t>(rp.rods * rp.m);
     if (t1 < t0) return fail(PSWIM_EINVAL, "propagate: t1 < t0");
     if (d_in != d_out) {
@@ -314,6 +316,7 @@ int pswim_ctx::propagate_graph(double t0, int scheme, int64_t steps, double dt, 
 // ---- space-parallel MRS (sharded targets, velocity all-gather) ------------------------
 int pswim_ctx::rhs_sharded(const pswim_transport* tr, const double* state, double t, double* u, double* w) {
     if (!has_scenario) return fail(PSWIM_EINVAL, "rhs: context has no scenario");
+    if (sc.wall_mode == 1) return fail(PSWIM_EUNSUPPORTED_WALL, kWallMsg);
     const bool lj = rp.rods >= 2 && rp.lj_well > 0.0;  // propagators.cpp:70
     if (lj) {
         const int rc = this->lj(state, d_lj);

@@ -8,6 +8,9 @@
 
 #include "internal.h"
 
+// stokes.cpp:15-17: the reference throws for image_wall (the correction is unspecified)
+inline constexpr const char* kWallMsg = "stokes: image_wall correction is not implemented; use free_space";
+
 struct pswim_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;

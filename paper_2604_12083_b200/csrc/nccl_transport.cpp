@@ -7,8 +7,9 @@
 //
 // NCCL is resolved at run time (dlopen) instead of at link time: the process may already
 // hold PyTorch's bundled libnccl.so.2 (a newer 2.28) and a link-time dependency on the
-// system 2.27 would otherwise shadow it.  Preference: an already-loaded libnccl.so.2, then
-// the CUDA wheel's copy, then the system library.
+// system 2.27 would otherwise shadow it.  Preference: an already-loaded libnccl.so.2 (torch's),
+// then $PSWIM_NCCL_LIB (the Python side points it at the running interpreter's nvidia-nccl
+// wheel), then the default loader search.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -41,15 +42,7 @@ NcclApi& api() {
         void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
         const char* env = std::getenv("PSWIM_NCCL_LIB");
         if (!h && env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
-        if (!h) {
-            const char* cands[] = {
-                "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2",
-                "libnccl.so.2",
-                "/usr/lib/x86_64-linux-gnu/libnccl.so.2",
-            };
-            for (const char* c : cands)
-                if ((h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
-        }
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);  // default loader search
         if (!h) return;
         a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
         a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));

@@ -185,6 +185,8 @@ int pswim_propagate_sharded_peer(pswim_ctx* ctx, pswim_peer_group* g, const doub
     int rc = ctx->use();
     if (rc) return rc;
     if (t1 < t0) return ctx->fail(PSWIM_EINVAL, "propagate: t1 < t0");
+    if (!ctx->has_scenario) return ctx->fail(PSWIM_EINVAL, "propagate: context has no scenario");
+    if (ctx->sc.wall_mode == 1) return ctx->fail(PSWIM_EUNSUPPORTED_WALL, kWallMsg);
     const size_t bytes = sizeof(double) * 12 * static_cast<size_t>(g->n);
     if (d_in != d_out && cudaMemcpyAsync(d_out, d_in, bytes, cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess)
         return ctx->fail(PSWIM_ECUDA, "propagate: copy");

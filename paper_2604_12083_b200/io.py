@@ -140,7 +140,7 @@ class RunRecord:
 
     def save(self, path: str) -> None:
         with open(path, "w") as fh:
-            fh.write(json.dumps(self.to_dict(), indent=2) + "\n")
+            fh.write(json.dumps(self.to_dict(), indent=2, sort_keys=True) + "\n")  # nlohmann dumps std::map order
 
 
 def write_schedule_csv(path: str, trace) -> None:

@@ -391,11 +391,29 @@ class StagedTransport:
             self.ptr = None
 
 
+def _point_at_wheel_nccl() -> None:
+    """libpswim dlopens NCCL: prefer the copy torch already loaded, else the nvidia-nccl wheel
+    of the running interpreter (PSWIM_NCCL_LIB), else the loader's default search."""
+    import os
+
+    if os.environ.get("PSWIM_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl as nv  # the CUDA wheel torch depends on
+
+        path = os.path.join(list(nv.__path__)[0], "lib", "libnccl.so.2")
+        if os.path.exists(path):
+            os.environ["PSWIM_NCCL_LIB"] = path
+    except Exception:
+        pass
+
+
 def nccl_transport(device: int):
     """NCCL transport for the current torch.distributed rank (unique id shared via the
     default process group)."""
     import torch.distributed as dist
 
+    _point_at_wheel_nccl()
     L = _lib.lib()
     rank, world = dist.get_rank(), dist.get_world_size()
     uid = (C.c_uint8 * 128)()
@@ -417,6 +435,7 @@ def nccl_group_transports(device: int, groups):
     its unique id, shared with one all_gather_object.  Returns {group index: transport}."""
     import torch.distributed as dist
 
+    _point_at_wheel_nccl()
     L = _lib.lib()
     rank = dist.get_rank()
     ids = {}

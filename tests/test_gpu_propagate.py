@@ -324,3 +324,19 @@ def test_fused_cluster_cap_bitwise(gpu):
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
     for c in (c16, c8, cl):
         c.close()
+
+
+@pytest.mark.parametrize("kw,steps", [(dict(rod_count=1, nodes_per_rod=21), 4),      # fused cluster path
+                                      (dict(rod_count=9, nodes_per_rod=64, epsilon=0.08), 40)])  # graph path
+def test_propagate_rejects_image_wall(gpu, kw, steps):
+    """image_wall throws in the reference (stokes.cpp:15-17) on every path, including the fused
+    and graph-replay propagates that never reach rhs()."""
+    from paper_2604_12083_b200 import PswimError
+    from paper_2604_12083_b200.propagators import StepperConfig, propagate
+    from paper_2604_12083_b200.scenario import build_initial_state
+
+    sc = scen(wall_mode=1, **kw)
+    x = build_initial_state(scen(**kw))
+    with pytest.raises(PswimError) as ei:
+        propagate(x, 0.0, steps * 1e-6, StepperConfig(0.0, 1, steps), sc)
+    assert ei.value.code == 2
