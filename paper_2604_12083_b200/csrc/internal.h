@@ -125,6 +125,15 @@ cudaError_t advance_launch(const RodParams& p, const double* state, const double
 cudaError_t sqrt_batched_launch(const double* r9, int64_t count, double* s9, cudaStream_t st);
 cudaError_t metric_launch(const double* x, const double* y, int64_t len, double* d_partial, int* d_count,
                           double* d_result, cudaStream_t st);
+// Many position metrics in one launch: d_result[p] = metric(x[p], y[p]) (rod_position_metric,
+// io.cpp:49-68), p < count <= kMetricPairs.
+constexpr int kMetricPairs = 128;
+struct MetricPairs {
+    int count = 0;
+    const double* x[kMetricPairs];
+    const double* y[kMetricPairs];
+};
+cudaError_t metric_pairs_launch(const MetricPairs& pairs, int64_t len, double* d_result, cudaStream_t st);
 cudaError_t correct_launch(const double* xp, const double* gn, const double* go, int64_t len, double* out,
                            cudaStream_t st);
 cudaError_t dfma_launch(double* sink, int blocks, int iters, cudaStream_t st);

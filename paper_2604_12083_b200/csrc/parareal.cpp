@@ -1,20 +1,10 @@
-// parareal.cpp — time-parallel drivers.
-//
-// (1) Engine: the physics-agnostic task-graph driver of parareal::run (reference
-//     include/pintswim/parareal.hpp:85-86, src/parareal.cpp:118-438): regular and pipelined
-//     schedules, worker lanes (serial lane 0 with priority, fine task n on lane
-//     1 + (n-1) % (m-1)), stop rule, iteration-ordered reports, schedule trace.  Backends:
-//       HostBackend  host states + C propagator callbacks  (pswim_parareal_run_host)
-//       GpuBackend   HBM states, one device context (stream) per worker lane, coarse =
-//                    Euler / fine = RK2 as harness::prepare (harness.cpp:5-33)
-//                                                           (pswim_parareal_run_gpu)
-// (2) RankDriver: one time slice per rank (rank p owns interval p+1, intervals == world),
-//     the same recurrence (parareal.cpp:58-89) with one state hand-off per iteration to
-//     rank p+1 and one allreduce(max) of [eta_tilde, eta] per iteration; coarse/corrector on
-//     a high-priority stream, fine on a low-priority stream; pipelined mode launches the
-//     next fine solve the moment its input arrives.  Transports: NCCL (one process per GPU,
-//     nccl_transport.cpp), in-process threads + peer copies (pswim_parareal_run_threads),
-//     host callbacks (CPU tests over gloo).
+// parareal.cpp — the time-sliced Parareal driver: one time slice per rank (rank p owns
+// interval p+1, intervals == world), the recurrence of src/parareal.cpp:58-89 with one state
+// hand-off per iteration to rank p+1 and one allreduce(max) of the iteration metric.
+// Coarse/corrector on a high-priority stream, fine on a low-priority stream, transport on a
+// third.  Transports: NCCL (one process per GPU, nccl_transport.cpp), in-process threads +
+// peer copies (pswim_parareal_run_threads), host callbacks (CPU tests over gloo).
+// The single-device engine (parareal::run itself) is engine.cpp.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -34,563 +24,7 @@
 #include <vector>
 
 #include "ctx.h"
-#include "internal.h"
-
-namespace pswim {
-namespace {
-
-using Clock = std::chrono::steady_clock;
-
-struct CodeError : std::runtime_error {
-    int code;
-    CodeError(int c, const std::string& w) : std::runtime_error(w), code(c) {}
-};
-
-int plan_check(const pswim_plan* p) {
-    // validate, parareal.cpp:38-45
-    if (!p || p->intervals < 1 || p->workers < 1) return PSWIM_EINVAL;
-    if (p->max_iterations < 1) return PSWIM_EINVAL;
-    if (!(p->tolerance > 0.0)) return PSWIM_EINVAL;
-    if (p->horizon <= 0.0) return PSWIM_EINVAL;
-    return PSWIM_OK;
-}
-
-// ParallelPlan::boundary_time, parareal.hpp:44 — every caller uses this expression so all
-// propagator calls see bitwise-identical interval ends.
-inline double boundary_time(const pswim_plan& p, int n) { return p.t0 + (p.horizon / p.intervals) * n; }
-
-// pointwise metric over groups: |x_i - y_i| / |x_i| on `dim` entries every `stride`
-// (parareal.cpp:15-34 with stride == dim; io.cpp:49-68 with dim 3, stride 12).
-double host_metric(const double* x, const double* y, int64_t len, int dim, int stride) {
-    double worst = 0.0;
-    for (int64_t i = 0; i < len; i += stride) {
-        double num = 0.0, den = 0.0;
-        for (int c = 0; c < dim; ++c) {
-            const double d = x[i + c] - y[i + c];
-            num += d * d;
-            den += x[i + c] * x[i + c];
-        }
-        num = std::sqrt(num);
-        den = std::sqrt(den);
-        worst = std::max(worst, den < 1e-14 ? num : num / den);
-    }
-    return worst;
-}
-
-// ---------------------------------------------------------------------------------------
-// Engine backends
-// ---------------------------------------------------------------------------------------
-struct State {
-    std::vector<double> host;
-    double* dev = nullptr;
-    std::function<void(double*)> release;
-    ~State() {
-        if (dev && release) release(dev);
-    }
-};
-using StatePtr = std::shared_ptr<const State>;
-
-class EngineBackend {
-  public:
-    virtual ~EngineBackend() = default;
-    virtual StatePtr initial(const double* x0) = 0;
-    // Runs on worker `w`'s thread; returns when the result is complete.
-    virtual StatePtr propagate(int w, bool coarse, double t0, double t1, const State& in) = 0;
-    // Driver thread.
-    virtual StatePtr corrected(const State& xp, const State& gn, const State& go) = 0;
-    virtual double metric(const State& x, const State& y) = 0;
-    virtual double metric_ref(const double* ref_host, const State& x) = 0;
-    virtual void download(const State& s, double* out) = 0;
-};
-
-class HostBackend final : public EngineBackend {
-  public:
-    HostBackend(int64_t len, pswim_propagator_fn c, void* cu, pswim_propagator_fn f, void* fu, int dim, int stride)
-        : len_(len), coarse_(c), cuser_(cu), fine_(f), fuser_(fu), dim_(dim), stride_(stride) {}
-    StatePtr initial(const double* x0) override {
-        auto s = std::make_shared<State>();
-        s->host.assign(x0, x0 + len_);
-        return s;
-    }
-    StatePtr propagate(int, bool coarse, double t0, double t1, const State& in) override {
-        auto s = std::make_shared<State>();
-        s->host.resize(len_);
-        const int rc = coarse ? coarse_(cuser_, t0, t1, in.host.data(), s->host.data(), len_, nullptr)
-                              : fine_(fuser_, t0, t1, in.host.data(), s->host.data(), len_, nullptr);
-        if (rc) throw CodeError(rc, "propagator failed");
-        return s;
-    }
-    StatePtr corrected(const State& xp, const State& gn, const State& go) override {
-        auto s = std::make_shared<State>();
-        s->host.resize(len_);
-        for (int64_t i = 0; i < len_; ++i) s->host[i] = xp.host[i] + gn.host[i] - go.host[i];  // parareal.cpp:52
-        return s;
-    }
-    double metric(const State& x, const State& y) override {
-        return host_metric(x.host.data(), y.host.data(), len_, dim_, stride_);
-    }
-    double metric_ref(const double* ref, const State& x) override {
-        return host_metric(ref, x.host.data(), len_, dim_, stride_);
-    }
-    void download(const State& s, double* out) override { std::memcpy(out, s.host.data(), len_ * sizeof(double)); }
-
-  private:
-    int64_t len_;
-    pswim_propagator_fn coarse_;
-    void* cuser_;
-    pswim_propagator_fn fine_;
-    void* fuser_;
-    int dim_, stride_;
-};
-
-// Fixed-size device buffer pool shared by every lane (all states have one size).
-class DevicePool {
-  public:
-    DevicePool(int device, int64_t len) : device_(device), bytes_(len * sizeof(double)) {}
-    ~DevicePool() {
-        cudaSetDevice(device_);
-        for (double* p : free_) cudaFree(p);
-    }
-    double* get() {
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            if (!free_.empty()) {
-                double* p = free_.back();
-                free_.pop_back();
-                return p;
-            }
-        }
-        cudaSetDevice(device_);
-        double* p = nullptr;
-        if (cudaMalloc(&p, bytes_) != cudaSuccess) throw CodeError(PSWIM_ECUDA, "parareal: out of device memory");
-        return p;
-    }
-    void put(double* p) {
-        std::lock_guard<std::mutex> lk(mu_);
-        free_.push_back(p);
-    }
-    size_t bytes() const { return bytes_; }
-    // Allocate up front (cudaMalloc inside a run would serialise against running kernels).
-    void reserve(int count) {
-        cudaSetDevice(device_);
-        std::lock_guard<std::mutex> lk(mu_);
-        for (int i = 0; i < count; ++i) {
-            double* p = nullptr;
-            if (cudaMalloc(&p, bytes_) != cudaSuccess) break;
-            free_.push_back(p);
-        }
-    }
-
-  private:
-    int device_;
-    size_t bytes_;
-    std::mutex mu_;
-    std::vector<double*> free_;
-};
-
-class GpuBackend final : public EngineBackend {
-  public:
-    GpuBackend(const pswim_scenario& sc, int device, int workers, int64_t fine_steps, int64_t coarse_steps,
-               int reserve_states)
-        : len_(12 * sc.rod_count * sc.nodes_per_rod), fine_steps_(fine_steps), coarse_steps_(coarse_steps) {
-        pool_ = std::make_shared<DevicePool>(device, len_);
-        pool_->reserve(reserve_states);
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        // lane 0 = serial wavefront (coarse + correctors): highest priority
-        for (int w = 0; w < workers; ++w) {
-            pswim_ctx* c = pswim_create(device, &sc, w == 0 ? hi : lo);
-            if (!c) throw CodeError(PSWIM_ECUDA, "parareal: cannot create worker context");
-            lanes_.push_back(c);
-        }
-        driver_ = pswim_create(device, nullptr, hi);
-        if (!driver_) throw CodeError(PSWIM_ECUDA, "parareal: cannot create driver context");
-    }
-    ~GpuBackend() override {
-        for (auto* c : lanes_) pswim_destroy(c);
-        pswim_destroy(driver_);
-    }
-    StatePtr make() {
-        auto s = std::make_shared<State>();
-        auto pool = pool_;
-        s->dev = pool->get();
-        s->release = [pool](double* p) { pool->put(p); };
-        return s;
-    }
-    StatePtr initial(const double* x0) override {
-        auto s = make();
-        driver_->use();
-        if (cudaMemcpy(s->dev, x0, pool_->bytes(), cudaMemcpyHostToDevice) != cudaSuccess)
-            throw CodeError(PSWIM_ECUDA, "parareal: upload");
-        return s;
-    }
-    StatePtr propagate(int w, bool coarse, double t0, double t1, const State& in) override {
-        auto s = make();
-        pswim_ctx* c = lanes_[w];
-        c->use();
-        int rc = c->propagate_async(in.dev, t0, t1, coarse ? PSWIM_EULER : PSWIM_RK2,
-                                    coarse ? coarse_steps_ : fine_steps_, 0.0, s->dev);
-        if (!rc) rc = c->sync();
-        if (rc) throw CodeError(rc, c->err);
-        return s;
-    }
-    StatePtr corrected(const State& xp, const State& gn, const State& go) override {
-        auto s = make();
-        driver_->use();
-        if (correct_launch(xp.dev, gn.dev, go.dev, len_, s->dev, driver_->stream) != cudaSuccess)
-            throw CodeError(PSWIM_ECUDA, "parareal: correct");
-        const int rc = driver_->sync();
-        if (rc) throw CodeError(rc, driver_->err);
-        return s;
-    }
-    double metric(const State& x, const State& y) override {
-        double v = 0.0;
-        const int rc = pswim_position_metric(driver_, x.dev, y.dev, len_, &v);
-        if (rc) throw CodeError(rc, driver_->err);
-        return v;
-    }
-    double metric_ref(const double* ref, const State& x) override {
-        return host_metric_vs(ref, x);
-    }
-    void download(const State& s, double* out) override {
-        driver_->use();
-        if (cudaMemcpy(out, s.dev, pool_->bytes(), cudaMemcpyDeviceToHost) != cudaSuccess)
-            throw CodeError(PSWIM_ECUDA, "parareal: download");
-    }
-
-  private:
-    double host_metric_vs(const double* ref, const State& x) {
-        std::vector<double> h(len_);
-        download(x, h.data());
-        return host_metric(ref, h.data(), len_, 3, 12);
-    }
-    int64_t len_, fine_steps_, coarse_steps_;
-    std::shared_ptr<DevicePool> pool_;
-    std::vector<pswim_ctx*> lanes_;
-    pswim_ctx* driver_ = nullptr;
-};
-
-// ---------------------------------------------------------------------------------------
-// Engine: task graph over slots (k, n), k = 0..L, n = 0..N.
-// ---------------------------------------------------------------------------------------
-enum Kind { kCoarse = 0, kFine = 1, kCorrect = 2, kIdle = 3 };
-
-struct Task {
-    Kind kind = kFine;
-    int k = 0, n = 0;
-    double t0 = 0, t1 = 0;
-    StatePtr input;
-};
-
-struct Done {
-    Task task;
-    StatePtr result;
-    std::exception_ptr error;
-};
-
-class Engine {
-  public:
-    Engine(const pswim_plan& plan, EngineBackend& be, const double* reference, int64_t len)
-        : plan_(plan), be_(be), ref_(reference), len_(len), N_(plan.intervals),
-          L_(std::min(plan.max_iterations, plan.intervals)), M_(plan.workers), lanes_(plan.workers),
-          lane_events_(plan.workers) {
-        const auto grid = [&](auto& v) { v.assign(L_ + 1, std::vector<typename std::decay_t<decltype(v)>::value_type::value_type>(N_ + 1)); };
-        grid(X_);
-        grid(G_);
-        grid(F_);
-        fine_sent_.assign(L_ + 1, std::vector<char>(N_ + 1, 0));
-        corr_sent_.assign(L_ + 1, std::vector<char>(N_ + 1, 0));
-        fines_left_.assign(L_ + 1, 0);
-        for (int k = 1; k <= L_; ++k) fines_left_[k] = N_ - k + 1;
-        slots_left_.assign(L_ + 1, N_);
-        iter_ready_.assign(L_ + 1, 0);
-    }
-
-    void run(const double* x0, double* states_out, pswim_report* rep, std::vector<pswim_trace_event>* trace) {
-        origin_ = Clock::now();
-        put_state(0, 0, be_.initial(x0));
-        // The sweep head is queued before any lane starts so lane 0's serial tier
-        // outranks a fine task seeded at t = 0 (parareal.cpp:147-151).
-        submit(Task{kCoarse, 0, 1, boundary_time(plan_, 0), boundary_time(plan_, 1), X_[0][0]});
-        notify_pending();
-        std::vector<std::thread> threads;
-        for (int w = 0; w < M_; ++w) threads.emplace_back([this, w] { lane_loop(w); });
-        while (outstanding_ > 0) {
-            Done d = next_done();
-            --outstanding_;
-            if (d.error && !failure_) {
-                failure_ = d.error;
-                halt_ = true;  // drain: a propagator failure aborts the run
-            }
-            if (!halt_ && d.result) {
-                try {
-                    on_done(d);
-                } catch (...) {
-                    if (!failure_) failure_ = std::current_exception();
-                    halt_ = true;
-                }
-            }
-            notify_pending();
-        }
-        for (auto& l : lanes_) {
-            std::lock_guard<std::mutex> lk(l.mu);
-            l.closed = true;
-            l.cv.notify_one();
-        }
-        for (auto& t : threads) t.join();
-        if (failure_) std::rethrow_exception(failure_);
-
-        const int kf = final_k_;
-        for (int n = 0; n <= N_; ++n) {
-            if (!X_[kf][n]) throw CodeError(PSWIM_ESTATE, "parareal: missing boundary state at termination");
-            be_.download(*X_[kf][n], states_out + len_ * n);
-        }
-        rep->iterations_used = report_iters_;
-        rep->converged = converged_ ? 1 : 0;
-        rep->eta_count = static_cast<int32_t>(eta_tilde_.size());
-        for (size_t k = 0; k < eta_tilde_.size(); ++k) {
-            rep->eta_tilde[k] = eta_tilde_[k];
-            if (rep->eta && ref_) rep->eta[k] = eta_[k];
-        }
-        if (trace) collect_trace(trace, rep);
-    }
-
-  private:
-    struct Lane {
-        std::mutex mu;
-        std::condition_variable cv;
-        std::deque<Task> serial, fine;
-        bool closed = false;
-    };
-
-    // ---- lanes ---------------------------------------------------------------------------
-    void lane_loop(int w) {
-        Lane& lane = lanes_[w];
-        for (;;) {
-            Task t;
-            {
-                std::unique_lock<std::mutex> lk(lane.mu);
-                lane.cv.wait(lk, [&] { return lane.closed || !lane.serial.empty() || !lane.fine.empty(); });
-                if (lane.serial.empty() && lane.fine.empty()) return;
-                std::deque<Task>& q = lane.serial.empty() ? lane.fine : lane.serial;
-                t = std::move(q.front());
-                q.pop_front();
-            }
-            Done d;
-            if (!halt_) {
-                try {
-                    const double a = since(Clock::now());
-                    d.result = be_.propagate(w, t.kind != kFine, t.t0, t.t1, *t.input);
-                    const double b = since(Clock::now());
-                    lane_events_[w].push_back(pswim_trace_event{w, static_cast<int32_t>(t.kind), a, b});
-                } catch (...) {
-                    d.error = std::current_exception();
-                }
-            }
-            d.task = std::move(t);
-            {
-                std::lock_guard<std::mutex> lk(done_mu_);
-                done_.push_back(std::move(d));
-            }
-            done_cv_.notify_one();
-        }
-    }
-
-    Done next_done() {
-        std::unique_lock<std::mutex> lk(done_mu_);
-        done_cv_.wait(lk, [&] { return !done_.empty(); });
-        Done d = std::move(done_.front());
-        done_.pop_front();
-        return d;
-    }
-
-    double since(Clock::time_point t) const { return std::chrono::duration<double>(t - origin_).count(); }
-
-    int lane_of(const Task& t) const {
-        if (t.kind != kFine) return 0;
-        return M_ >= 2 ? 1 + (t.n - 1) % (M_ - 1) : 0;
-    }
-
-    void submit(Task t) {
-        const int w = lane_of(t);
-        ++outstanding_;
-        {
-            std::lock_guard<std::mutex> lk(lanes_[w].mu);
-            (t.kind == kFine ? lanes_[w].fine : lanes_[w].serial).push_back(std::move(t));
-        }
-        wake_.push_back(w);
-    }
-
-    // Tasks created while handling one completion are queued together and the lanes woken
-    // afterwards, so a waking lane sees this round's serial task before its fine task.
-    void notify_pending() {
-        for (int w : wake_) lanes_[w].cv.notify_one();
-        wake_.clear();
-    }
-
-    // ---- driver --------------------------------------------------------------------------
-    void on_done(const Done& d) {
-        const Task& t = d.task;
-        if (t.kind == kCoarse) {
-            G_[0][t.n] = d.result;
-            put_state(0, t.n, d.result);
-            try_correct(1, t.n);
-            if (t.n < N_ && !halt_)
-                submit(Task{kCoarse, 0, t.n + 1, boundary_time(plan_, t.n), boundary_time(plan_, t.n + 1), X_[0][t.n]});
-        } else if (t.kind == kFine) {
-            F_[t.k][t.n] = d.result;
-            --fines_left_[t.k];
-            if (t.n == t.k)
-                put_state(t.k, t.k, d.result);  // X_k^k = fine result
-            else
-                try_correct(t.k, t.n);
-            if (plan_.mode == 0 && fines_left_[t.k] == 0) try_correct(t.k, t.k + 1);
-        } else {
-            G_[t.k][t.n] = d.result;
-            put_state(t.k, t.n, be_.corrected(*F_[t.k][t.n], *d.result, *G_[t.k - 1][t.n]));
-            try_correct(t.k + 1, t.n);
-        }
-    }
-
-    void put_state(int k, int n, const StatePtr& v) {
-        if (X_[k][n]) return;
-        X_[k][n] = v;
-        if (n >= 1 && --slots_left_[k] == 0) {
-            iter_ready_[k] = 1;
-            // reports come out in iteration order even when speculative pipelined work
-            // finishes a later iteration first
-            while (next_report_ <= L_ && iter_ready_[next_report_] && !halt_) finish_iteration(next_report_++);
-            if (halt_) return;
-        }
-        if (n + 1 <= N_) try_correct(k, n + 1);
-        if (k + 1 <= L_) {
-            if (n <= k) put_state(k + 1, n, v);          // converged prefix is frozen
-            if (plan_.mode == 1 && n >= k + 1) try_fine(k + 1, n);  // streaming hand-off
-        }
-    }
-
-    void try_fine(int k, int n) {
-        if (halt_ || k > L_ || n < k || n > N_ || fine_sent_[k][n] || !X_[k - 1][n - 1]) return;
-        fine_sent_[k][n] = 1;
-        submit(Task{kFine, k, n, boundary_time(plan_, n - 1), boundary_time(plan_, n), X_[k - 1][n - 1]});
-    }
-
-    void try_correct(int k, int n) {
-        if (halt_ || k < 1 || k > L_ || n < k + 1 || n > N_ || corr_sent_[k][n]) return;
-        if (!F_[k][n] || !X_[k][n - 1] || !G_[k - 1][n]) return;
-        if (plan_.mode == 0 && fines_left_[k] > 0) return;
-        corr_sent_[k][n] = 1;
-        submit(Task{kCorrect, k, n, boundary_time(plan_, n - 1), boundary_time(plan_, n), X_[k][n - 1]});
-    }
-
-    void finish_iteration(int k) {
-        if (k == 0) {
-            if (plan_.mode == 0)
-                for (int n = 1; n <= N_; ++n) try_fine(1, n);
-            return;
-        }
-        double et = 0.0, e = 0.0;
-        for (int n = 1; n <= N_; ++n) {
-            et = std::max(et, be_.metric(*X_[k][n], *X_[k - 1][n]));
-            if (ref_) e = std::max(e, be_.metric_ref(ref_ + len_ * n, *X_[k][n]));
-        }
-        eta_tilde_.push_back(et);
-        if (ref_) eta_.push_back(e);
-        report_iters_ = k;
-        if (et < plan_.tolerance || k == N_) {
-            converged_ = true;  // at k = n every interval is exact (parareal.cpp:383-386)
-            halt_at(k);
-        } else if (k == L_) {
-            halt_at(k);
-        } else if (plan_.mode == 0) {
-            for (int n = k + 1; n <= N_; ++n) try_fine(k + 1, n);
-        }
-    }
-
-    void halt_at(int k) {
-        final_k_ = k;
-        halt_ = true;
-    }
-
-    void collect_trace(std::vector<pswim_trace_event>* out, pswim_report* rep) {
-        // ScheduleTrace::finalize_idle (schedule_trace.cpp:17-41): idle gaps on every lane but
-        // the serial one, from t = 0 to each task start.
-        std::vector<pswim_trace_event> ev;
-        for (auto& l : lane_events_) ev.insert(ev.end(), l.begin(), l.end());
-        auto order = [](const pswim_trace_event& a, const pswim_trace_event& b) {
-            return a.worker != b.worker ? a.worker < b.worker : a.t_start < b.t_start;
-        };
-        std::stable_sort(ev.begin(), ev.end(), order);
-        std::vector<pswim_trace_event> gaps;
-        double cursor = 0.0, idle = 0.0;
-        int cur = -1;
-        for (const auto& e : ev) {
-            if (e.worker != cur) {
-                cur = e.worker;
-                cursor = 0.0;
-            }
-            if (e.worker != 0 && e.t_start > cursor) {
-                gaps.push_back(pswim_trace_event{e.worker, kIdle, cursor, e.t_start});
-                idle += e.t_start - cursor;
-            }
-            cursor = std::max(cursor, e.t_end);
-        }
-        ev.insert(ev.end(), gaps.begin(), gaps.end());
-        std::stable_sort(ev.begin(), ev.end(), order);
-        *out = std::move(ev);
-        rep->schedule_idle = idle;
-    }
-
-    const pswim_plan plan_;
-    EngineBackend& be_;
-    const double* ref_;
-    const int64_t len_;
-    const int N_, L_, M_;
-    std::vector<std::vector<StatePtr>> X_, G_, F_;
-    std::vector<std::vector<char>> fine_sent_, corr_sent_;
-    std::vector<int> fines_left_, slots_left_;
-    std::vector<char> iter_ready_;
-    int next_report_ = 0;
-    std::vector<Lane> lanes_;
-    std::vector<std::vector<pswim_trace_event>> lane_events_;
-    std::mutex done_mu_;
-    std::condition_variable done_cv_;
-    std::deque<Done> done_;
-    std::vector<int> wake_;
-    std::atomic<bool> halt_{false};
-    std::exception_ptr failure_;
-    int outstanding_ = 0;
-    int final_k_ = 0;
-    Clock::time_point origin_;
-    std::vector<double> eta_tilde_, eta_;
-    int report_iters_ = 0;
-    bool converged_ = false;
-};
-
-int run_engine(const pswim_plan* plan, EngineBackend& be, const double* x0, int64_t len, const double* ref,
-               double* states_out, pswim_report* rep, pswim_trace_event* trace_out, int64_t trace_cap,
-               int64_t* trace_len) {
-    const auto t0 = Clock::now();
-    try {
-        Engine eng(*plan, be, ref, len);
-        std::vector<pswim_trace_event> trace;
-        eng.run(x0, states_out, rep, &trace);
-        if (trace_len) *trace_len = static_cast<int64_t>(trace.size());
-        if (trace_out) {
-            const int64_t n = std::min<int64_t>(trace_cap, static_cast<int64_t>(trace.size()));
-            std::copy(trace.begin(), trace.begin() + n, trace_out);
-        }
-    } catch (const CodeError& e) {
-        return e.code;
-    } catch (const std::exception&) {
-        return PSWIM_ESTATE;
-    }
-    rep->wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
-    return PSWIM_OK;
-}
-
-}  // namespace
-}  // namespace pswim
+#include "parareal_common.h"
 
 // =========================================================================================
 // Rank driver (one slice per rank)
@@ -1214,36 +648,6 @@ struct HubBundle {
 // C ABI
 // =========================================================================================
 extern "C" {
-
-int pswim_parareal_run_host(const pswim_plan* plan, pswim_propagator_fn coarse, void* cu, pswim_propagator_fn fine,
-                            void* fu, const double* x0, int64_t len, int32_t dim, int32_t stride,
-                            const double* reference, double* states_out, pswim_report* rep,
-                            pswim_trace_event* trace_out, int64_t trace_cap, int64_t* trace_len) {
-    using namespace pswim;
-    if (plan_check(plan) || !coarse || !fine || !x0 || !states_out || !rep || len <= 0) return PSWIM_EINVAL;
-    if (dim < 1 || stride < dim || len % stride != 0) return PSWIM_EINVAL;
-    HostBackend be(len, coarse, cu, fine, fu, dim, stride);
-    return run_engine(plan, be, x0, len, reference, states_out, rep, trace_out, trace_cap, trace_len);
-}
-
-int pswim_parareal_run_gpu(const pswim_plan* plan, const pswim_scenario* sc, int device, int64_t fine_steps,
-                           int64_t coarse_steps, const double* x0, const double* reference, double* states_out,
-                           pswim_report* rep, pswim_trace_event* trace_out, int64_t trace_cap, int64_t* trace_len) {
-    using namespace pswim;
-    if (plan_check(plan) || !sc || !x0 || !states_out || !rep || fine_steps < 1 || coarse_steps < 1)
-        return PSWIM_EINVAL;
-    try {
-        const int L = std::min(plan->max_iterations, plan->intervals);
-        // X, G, F slots of the task graph (+1 input); bounded so huge states do not exhaust HBM
-        const int64_t want = 3LL * (L + 1) * (plan->intervals + 1) + 1;
-        const int64_t cap = (int64_t)((8ULL << 30) / (sizeof(double) * 12ULL * sc->rod_count * sc->nodes_per_rod));
-        GpuBackend be(*sc, device, plan->workers, fine_steps, coarse_steps, (int)std::min<int64_t>(want, cap));
-        return run_engine(plan, be, x0, 12 * sc->rod_count * sc->nodes_per_rod, reference, states_out, rep, trace_out,
-                          trace_cap, trace_len);
-    } catch (const CodeError& e) {
-        return e.code;
-    }
-}
 
 int pswim_parareal_rank_gpu(const pswim_plan* plan, const pswim_scenario* sc, int device, const pswim_transport* tr,
                             int64_t fine_steps, int64_t coarse_steps, const double* x0, const double* ref_slice,

@@ -396,6 +396,36 @@ __global__ void metric_kernel(const double* __restrict__ x, const double* __rest
     if ((threadIdx.x & 31) == 0) atomicMax(result, (unsigned long long)__double_as_longlong(worst));
 }
 
+// Position metric of many (x, y) state pairs in one launch (one Parareal iteration's
+// eta_tilde and eta columns): pair p = blockIdx.y, same per-node arithmetic as metric_kernel.
+__global__ void metric_pairs_kernel(const __grid_constant__ MetricPairs pairs, int64_t nodes,
+                                    unsigned long long* __restrict__ result) {
+    const double* x = pairs.x[blockIdx.y];
+    const double* y = pairs.y[blockIdx.y];
+    double worst = 0.0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nodes; k += (int64_t)gridDim.x * blockDim.x) {
+        const double* a = x + 12 * k;
+        const double* c = y + 12 * k;
+        double num = 0.0, den = 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const double d = a[q] - c[q];
+            num += d * d;
+            den += a[q] * a[q];
+        }
+        num = sqrt(num);
+        den = sqrt(den);
+        const double v = den < 1e-14 ? num : num / den;
+        worst = worst < v ? v : worst;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double other = __shfl_xor_sync(0xffffffffu, worst, o);
+        worst = worst < other ? other : worst;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(result + blockIdx.y, (unsigned long long)__double_as_longlong(worst));
+}
+
 __global__ void correct_kernel(const double* __restrict__ xp, const double* __restrict__ gn,
                                const double* __restrict__ go, int64_t len, double* __restrict__ out) {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < len; k += (int64_t)gridDim.x * blockDim.x) {
@@ -493,6 +523,7 @@ void rod_preload() {
     cudaFuncGetAttributes(&a, sqrt_plain_kernel);
     cudaFuncGetAttributes(&a, metric_kernel);
     cudaFuncGetAttributes(&a, correct_kernel);
+    cudaFuncGetAttributes(&a, metric_pairs_kernel);
     cudaFuncGetAttributes(&a, advance_kernel);
     cudaFuncGetAttributes(&a, advance_tma_kernel);
 }
@@ -553,6 +584,17 @@ cudaError_t metric_launch(const double* x, const double* y, int64_t len, double*
     const int64_t nodes = len / 12;
     const unsigned blocks = (unsigned)std::min<int64_t>(grid_for(nodes, 256), 1184);
     metric_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(x, y, nodes, reinterpret_cast<unsigned long long*>(d_result));
+    return cudaGetLastError();
+}
+
+cudaError_t metric_pairs_launch(const MetricPairs& pairs, int64_t len, double* d_result, cudaStream_t st) {
+    if (pairs.count <= 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(d_result, 0, pairs.count * sizeof(double), st);
+    if (e != cudaSuccess) return e;
+    const int64_t nodes = len / 12;
+    const unsigned bx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(nodes, 256), 64));
+    metric_pairs_kernel<<<dim3(bx, pairs.count), 256, 0, st>>>(pairs, nodes,
+                                                               reinterpret_cast<unsigned long long*>(d_result));
     return cudaGetLastError();
 }
 
