@@ -41,6 +41,9 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# more hardware work queues than the default 8, so that the streams of one process (coarse,
+# fine, comm, engine lanes) do not serialise behind each other's device-side waits
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 N_POINTS = 16384
 EPS, MU = 0.1, 1.0
@@ -48,11 +51,47 @@ FLOP_PER_PAIR = 103
 WORKLOAD = "MRS all-pairs velocity evaluation, N=16384 regularized points (BASELINE configs[1])"
 
 
+class Mt19937_64:
+    """std::mt19937_64 (the C++ standard's 64-bit Mersenne Twister), so the bench draws exactly
+    the inputs of the reference's own timer (tools/bench_kernels.cpp:46-50)."""
+
+    N, M = 312, 156
+    MASK = (1 << 64) - 1
+
+    def __init__(self, seed: int = 5489):
+        mt = [seed & self.MASK]
+        for i in range(1, self.N):
+            mt.append((6364136223846793005 * (mt[-1] ^ (mt[-1] >> 62)) + i) & self.MASK)
+        self.mt, self.i = mt, self.N
+
+    def _twist(self):
+        mt, n, m = self.mt, self.N, self.M
+        for i in range(n):
+            x = (mt[i] & 0xFFFFFFFF80000000) | (mt[(i + 1) % n] & 0x7FFFFFFF)
+            xa = x >> 1
+            if x & 1:
+                xa ^= 0xB5026F5AA96619E9
+            mt[i] = mt[(i + m) % n] ^ xa
+        self.i = 0
+
+    def __call__(self) -> int:
+        if self.i >= self.N:
+            self._twist()
+        y = self.mt[self.i]
+        self.i += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & self.MASK
+
+
 def synthetic_inputs(n: int, seed: int):
-    """x, f, n i.i.d. U[-0.5, 0.5)^3 drawn per point in that order (bench_kernels.cpp:46-63
-    with numpy's generator instead of mt19937_64)."""
-    rng = np.random.default_rng(seed)
-    u = rng.random((n, 3, 3)) - 0.5
+    """x, f, n per point in that order, each component (rng() >> 11) * 2^-53 - 0.5 from
+    std::mt19937_64(seed) -- bench_kernels.cpp:46-50 / :59-63 (seed 7 there)."""
+    rng = Mt19937_64(seed)
+    u = np.array([rng() >> 11 for _ in range(9 * n)], dtype=np.float64) * 2.0 ** -53 - 0.5
+    u = u.reshape(n, 3, 3)
     return [np.ascontiguousarray(u[:, i, :]) for i in range(3)]
 
 
@@ -156,15 +195,24 @@ def barrier():
 
 
 # ------------------------------------------------------------------------------------------
+_INPUTS = {}
+
+
+def inputs_cached(n: int, seed: int):
+    if (n, seed) not in _INPUTS:
+        _INPUTS[n, seed] = synthetic_inputs(n, seed)
+    return _INPUTS[n, seed]
+
+
 def cpu_reference_mrs(n_targets: int, reps: int, threads: int | None = None):
     """The reference's evaluate_velocities (OpenMP) on n_targets x N_POINTS pairs."""
     from oracle.pyoracle import Oracle
 
     ref = Oracle("ref")
-    if threads:
-        ref.set_threads_(threads)
+    full = ref.max_threads_()
+    ref.set_threads_(threads or full)
     cores = ref.max_threads_()
-    x, f, tq = synthetic_inputs(N_POINTS, 7)
+    x, f, tq = inputs_cached(N_POINTS, 7)
     tgt = np.ascontiguousarray(x[:n_targets])
     ref.evaluate_velocities(tgt[:64], x, f, tq, EPS, MU, parallel=True)  # OpenMP team warm-up
     times = []
@@ -172,10 +220,15 @@ def cpu_reference_mrs(n_targets: int, reps: int, threads: int | None = None):
         t0 = time.perf_counter()
         ref.evaluate_velocities(tgt, x, f, tq, EPS, MU, parallel=True)
         times.append(time.perf_counter() - t0)
+    ref.set_threads_(full)
     return times, cores
 
 
 def run_reference_arm(args) -> None:
+    """The reference's own evaluate_velocities (oracle/_ref, OpenMP, every host thread) on the
+    SAME workload as our arm: the full N x N evaluation of the same mt19937_64(7) inputs, each
+    step one evaluation.  Also one evaluation with a single thread (the reference's serial
+    path cost), with the host's core count."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
@@ -184,13 +237,22 @@ def run_reference_arm(args) -> None:
     t = times[args.warmup:] or times
     per = sum(t) / len(t)
     value = n_targets * N_POINTS / per / 1e9
-    sample = f"{n_targets} targets x {N_POINTS} sources per step (bounded sample of the N=16384 all-pairs workload)"
+    one, _ = cpu_reference_mrs(n_targets, 1, threads=1)
+    sample = (f"{n_targets} targets x {N_POINTS} sources per step" +
+              (" (the full all-pairs evaluation of our arm's workload)" if n_targets == N_POINTS else
+               " (bounded sample of the N=16384 all-pairs workload)"))
     line = {
         "impl": "reference", "metric": "MRS Gpair-interactions/s", "value": value, "unit": "Gpair/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * per,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "points": N_POINTS, "epsilon": EPS, "mu": MU, "l2": "n/a (CPU)"},
-        "cpu_baseline": {"value": value, "unit": "Gpair/s", "cores": cores, "kind": "reference", "sample": sample},
+        "config": {"workload": WORKLOAD, "points": N_POINTS, "epsilon": EPS, "mu": MU, "targets_equal_sources": True,
+                   "inputs": "std::mt19937_64(7), (rng() >> 11) * 2^-53 - 0.5 per component (bench_kernels.cpp:46-50)",
+                   "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": value, "unit": "Gpair/s", "cores": cores, "kind": "reference", "sample": sample,
+                         "nproc": os.cpu_count(),
+                         "single_thread": {"value": n_targets * N_POINTS / one[0] / 1e9, "unit": "Gpair/s",
+                                           "cores": 1, "sample": "one evaluation of the same workload, "
+                                                                 "OMP team of 1 thread"}},
         "e2e": {"value": value, "unit": "Gpair/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -224,8 +286,8 @@ def run_ours(args) -> None:
     # --- measured FP64 peak (roofline denominator) ---
     dfma_peak, _ = ctx.dfma_peak()
 
-    # --- device-resident inputs ---
-    x, f, tq = synthetic_inputs(n, 7 + rank)
+    # --- device-resident inputs (every rank its own suspension of the same size) ---
+    x, f, tq = inputs_cached(n, 7 + rank)
     dx, df, dn = (torch.as_tensor(a, device=dev) for a in (x, f, tq))
     du = torch.empty_like(dx)
     dw = torch.empty_like(dx)
@@ -316,6 +378,14 @@ def run_ours(args) -> None:
                 "flop_per_pair": FLOP_PER_PAIR, "peak_source": "DFMA microbenchmark measured in this run "
                 "(MEASURED_PEAKS.json has no FP64 entry)", "dp_instructions_per_pair_loop": 51}
 
+    # --- the north_star's MRS target sizes (N >= 64k), rank 0 at N = 1 ---
+    sweep = None
+    if rank == 0 and world == 1 and not args.no_sweep:
+        try:
+            sweep = mrs_sweep_leg(ctx, L, kp, dev, local, dfma_peak, flush)
+        except Exception as e:
+            sweep = {"error": f"{type(e).__name__}: {e}"}
+
     # --- secondary: simulated RK2 time-steps/s ---
     time_steps = None
     if not args.no_steps:
@@ -354,8 +424,9 @@ def run_ours(args) -> None:
             ct, cores = cpu_reference_mrs(nt, 3)
             best = min(ct)
             cpu = {"value": nt * n / best / 1e9, "unit": "Gpair/s", "cores": cores, "kind": "reference",
-                   "sample": f"best of 3: {nt} targets x {n} sources of the N=16384 workload "
-                             "(oracle/_ref = reference evaluate_velocities, OpenMP)"}
+                   "nproc": os.cpu_count(),
+                   "sample": f"best of 3: {nt} targets x {n} sources of the N=16384 workload, the same "
+                             "mt19937_64(7) inputs (oracle/_ref = reference evaluate_velocities, OpenMP)"}
         else:
             cpu = {"value": None, "unit": "Gpair/s", "cores": 0, "kind": "reference",
                    "sample": "oracle/_ref not built on this box"}
@@ -375,6 +446,7 @@ def run_ours(args) -> None:
             "roofline": roofline,
             "cpu_baseline": cpu,
             "parity_rel_err_vs_oracle": parity,
+            "mrs_sweep": sweep,
             "time_steps": time_steps,
             "hbm_kernels": hbm,
         }
@@ -383,6 +455,52 @@ def run_ours(args) -> None:
     if world > 1:
         barrier()
         dist.destroy_process_group()
+
+
+def mrs_sweep_leg(ctx, L, kp, dev, local, dfma_peak, flush, sizes=(65536, 131072), reps=5):
+    """MRS at the north_star's sizes (>= 60 % of FP64 peak at N >= 64k): same inputs recipe
+    (mt19937_64(7)), targets = sources, L2 flushed before every timed launch, CUDA events on
+    the launching stream, clocks sampled during the timed launches."""
+    import torch
+
+    from paper_2604_12083_b200.device import dptr
+
+    st = ctx.torch_stream()
+    out = {"workload": "MRS all-pairs evaluation, targets = sources, eps=0.1, mu=1, mt19937_64(7) inputs "
+                       "(BASELINE configs[1] recipe at the north_star's N >= 64k)", "points": {}}
+    for n in sizes:
+        x, f, tq = inputs_cached(n, 7)
+        dx, df, dn = (torch.as_tensor(a, device=dev) for a in (x, f, tq))
+        du, dw = torch.empty_like(dx), torch.empty_like(dx)
+
+        def launch():
+            ctx.check(L.pswim_mrs_velocities(ctx.handle, dptr(dx), n, dptr(dx), dptr(df), dptr(dn), n, C.byref(kp),
+                                             dptr(du), dptr(dw)))
+
+        for _ in range(3):
+            launch()
+        ctx.sync()
+        times = []
+        with ClockSampler(local) as clk:
+            for _ in range(reps):
+                with torch.cuda.stream(st):
+                    flush.zero_()
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                launch()
+                b.record(st)
+                b.synchronize()
+                times.append(a.elapsed_time(b))
+        ctx.sync()
+        ms = sum(times) / len(times)
+        achieved = FLOP_PER_PAIR * n * n / (ms * 1e-3) / 1e12
+        out["points"][str(n)] = {"value": n * n / (ms * 1e-3) / 1e9, "unit": "Gpair/s", "ms": ms,
+                                 "roofline_frac": achieved / (dfma_peak / 1e12), "achieved_tflops": achieved,
+                                 "clocks": clk.summary(), "launches": reps}
+        del dx, df, dn, du, dw
+    out["peak_tflops"] = dfma_peak / 1e12
+    return out
 
 
 def time_steps_leg(args, world, rank, local, dev):
@@ -400,7 +518,7 @@ def time_steps_leg(args, world, rank, local, dev):
         L = ctx.lib
         dx = torch.as_tensor(x0, device=dev)
         out = torch.empty_like(dx)
-        steps = args.fine_steps
+        steps = args.serial_steps
         ctx.check(L.pswim_propagate(ctx.handle, dptr(dx), 0.0, 3e-6, 1, 3, 0.0, dptr(out)))  # warm-up
         st = ctx.torch_stream()
         a = torch.cuda.Event(enable_timing=True)
@@ -427,43 +545,15 @@ def time_steps_leg(args, world, rank, local, dev):
                                        "kind": "reference",
                                        "sample": "2 RK2 steps of the same suspension (reference propagate, OpenMP)"}
         leg["flagellum"] = flagellum_leg(args, local, dev)
+        try:
+            leg["gpu_vs_reference_parareal"] = reduced_parity(local)
+        except Exception as e:
+            leg["gpu_vs_reference_parareal"] = {"error": f"{type(e).__name__}: {e}"}
         return leg
-    # N > 1: one Parareal slice per GPU, NCCL hand-offs
-    fine_steps, coarse_steps = args.fine_steps, max(1, args.fine_steps // 10)
-    plan = pr.ParallelPlan(t0=0.0, horizon=world * fine_steps * 1e-6, intervals=world, workers=world,
-                           max_iterations=args.parareal_iters, tolerance=1e-300, mode=pr.PIPELINED)
+    # N > 1: one Parareal slice per GPU (BASELINE configs[3])
     tr = _transport(local)
     try:
-        pr.run_sliced_rank(plan, sc, fine_steps, coarse_steps, x0, local, transport=tr)  # warm-up
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        res = pr.run_sliced_rank(plan, sc, fine_steps, coarse_steps, x0, local, transport=tr)
-        wall = reduce_max(time.perf_counter() - t0, dev)
-        # the same fine propagation serially on one GPU (rank 0), for the speedup
-        serial = None
-        barrier()
-        if rank == 0:
-            from paper_2604_12083_b200.device import Context, dptr
-
-            sctx = Context(local, sc)
-            dx = torch.as_tensor(x0, device=dev)
-            dout = torch.empty_like(dx)
-            sctx.check(sctx.lib.pswim_propagate(sctx.handle, dptr(dx), 0.0, fine_steps * 1e-6, 1, fine_steps, 0.0,
-                                                dptr(dout)))
-            torch.cuda.synchronize()
-            t1 = time.perf_counter()
-            sctx.check(sctx.lib.pswim_propagate(sctx.handle, dptr(dx), 0.0, fine_steps * 1e-6, 1, fine_steps, 0.0,
-                                                dptr(dout)))
-            serial = world * (time.perf_counter() - t1)  # n intervals of serial fine
-            sctx.close()
-        barrier()
-        leg = {"metric": "simulated RK2 time-steps/s", "value": world * fine_steps / wall, "unit": "steps/s",
-               "speedup_vs_serial_fine": (serial / wall) if serial else None,
-               "config": {"workload": "pipelined Parareal, one slice per GPU, 64 x 256 suspension (BASELINE configs[3])",
-                          "intervals": world, "fine_rk2_steps_per_interval": fine_steps,
-                          "coarse_euler_steps_per_interval": coarse_steps, "iterations": res.report.iterations_used,
-                          "eta_tilde": res.report.eta_tilde}}
+        leg = parareal_sweep_leg(args, sc, x0, world, rank, local, dev, tr)
         try:
             leg["space_parallel"] = space_parallel_leg(sc, x0, local, dev, tr, world)
         except Exception as e:
@@ -481,6 +571,138 @@ def time_steps_leg(args, world, rank, local, dev):
     finally:
         _lib_destroy(tr)
     return leg
+
+
+def serial_fine_boundaries_gpu(sc, x0, plan, fine, local, dev):
+    """harness::serial_fine_boundaries (harness.cpp:35-37) on one GPU: the fine propagator
+    chained over the plan's intervals at boundary_time(n).  Returns (states, seconds)."""
+    import torch
+
+    from paper_2604_12083_b200.device import Context, dptr
+
+    ctx = Context(local, sc)
+    cur = torch.as_tensor(x0, device=dev)
+    nxt = torch.empty_like(cur)
+    ctx.check(ctx.lib.pswim_propagate(ctx.handle, dptr(cur), 0.0, 2e-6, 1, 2, 0.0, dptr(nxt)))  # warm-up
+    states = [cur.clone()]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(plan.intervals):
+        ctx.check(ctx.lib.pswim_propagate(ctx.handle, dptr(cur), plan.boundary_time(i), plan.boundary_time(i + 1), 1,
+                                          fine, 0.0, dptr(nxt)))
+        cur, nxt = nxt, cur
+        states.append(cur.clone())
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t0
+    ctx.close()
+    return states, sec
+
+
+def parareal_sweep_leg(args, sc, x0, world, rank, local, dev, tr):
+    """BASELINE configs[3] as BASELINE.md states it: n = m = world intervals of `fine` RK2 steps
+    (dt = 1e-6) with `coarse` Euler steps (r = 2 fine / coarse rhs), pipelined Parareal with one
+    slice per GPU, l = 1..min(4, world) at tol = 1e-300 (fixed l) and one tol = 1e-10 run.  Per
+    run: simulated steps/s, speedup over the 1-GPU serial fine integration of the same horizon,
+    eta = true error vs that serial fine solution (max over ranks, rod_position_metric), and the
+    schedule idle W of the rank-driver trace."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_12083_b200 import parareal as pr
+
+    fine, coarse = args.fine_steps, max(1, min(args.coarse_steps, args.fine_steps // 10))
+    T = world * fine * 1e-6
+
+    def plan(l, tol=1e-300):
+        return pr.ParallelPlan(t0=0.0, horizon=T, intervals=world, workers=world, max_iterations=l, tolerance=tol,
+                               mode=pr.PIPELINED)
+
+    # serial fine on rank 0: the speedup denominator and every rank's true-error reference
+    barrier()
+    buf = torch.empty((world + 1, x0.size), dtype=torch.float64, device=dev if WIRE == "nccl" else "cpu")
+    serial = torch.zeros(1, dtype=torch.float64, device=buf.device)
+    if rank == 0:
+        states, sec = serial_fine_boundaries_gpu(sc, x0, plan(1), fine, local, dev)
+        buf.copy_(torch.stack(states))
+        serial.fill_(sec)
+    dist.broadcast(buf, 0)
+    dist.broadcast(serial, 0)
+    serial_s = float(serial.item())
+    ref_slice = buf[rank + 1].cpu().numpy()
+    warm = pr.ParallelPlan(t0=0.0, horizon=world * 1e-6, intervals=world, workers=world, max_iterations=1,
+                           tolerance=1e-300, mode=pr.PIPELINED)
+    pr.run_sliced_rank(warm, sc, 1, 1, x0, local, transport=tr)  # contexts, kernels, plans
+
+    def timed(p, handoff=None):
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = pr.run_sliced_rank(p, sc, fine, coarse, x0, local, transport=tr, reference_slice=ref_slice,
+                                 handoff=handoff)
+        wall = reduce_max(time.perf_counter() - t0, dev)
+        eta = res.report.eta[-1] if res.report.eta else None
+        return res, {"iterations": res.report.iterations_used, "converged": res.report.converged,
+                     "value": world * fine / wall, "unit": "steps/s", "wall_s": wall,
+                     "speedup_vs_serial_fine": serial_s / wall, "eta_vs_serial_fine": eta,
+                     "within_tolerance_1e-10": eta is not None and eta <= 1e-10,
+                     "eta_tilde": res.report.eta_tilde, "schedule_idle_s": res.schedule_idle}
+
+    sweep = [timed(plan(l))[1] for l in range(1, min(4, world) + 1)]
+    _, tol_run = timed(plan(world, 1e-10))
+    leg = {"metric": "simulated RK2 time-steps/s", "value": tol_run["value"], "unit": "steps/s",
+           "speedup_vs_serial_fine": tol_run["speedup_vs_serial_fine"],
+           "eta_vs_serial_fine": tol_run["eta_vs_serial_fine"],
+           "config": {"workload": "pipelined Parareal, one slice per GPU, 64 x 256 suspension, eps=0.08, dt=1e-6 "
+                                  "(BASELINE configs[3]); headline = the tol=1e-10 run", "intervals": world,
+                      "fine_rk2_steps_per_interval": fine, "coarse_euler_steps_per_interval": coarse,
+                      "cost_ratio_r": 2.0 * fine / coarse, "tolerance": 1e-10,
+                      "iterations": tol_run["iterations"], "eta_tilde": tol_run["eta_tilde"]},
+           "serial_fine_s": serial_s, "serial_fine_steps_per_s": world * fine / serial_s,
+           "speedup_denominator": "1-GPU serial fine integration of the same world x fine RK2 steps, measured",
+           "tolerance_run": tol_run, "iteration_sweep": sweep}
+    # the same l = 2 run with the peer-memory hand-off (corrector stores into the next rank's
+    # HBM slot over NVLink, CUDA IPC) instead of NCCL send/recv
+    try:
+        ho = pr.Handoff(local, x0.size, min(2, world) + 1)
+        barrier()
+        _, hrun = timed(plan(min(2, world)), handoff=ho)
+        barrier()
+        ho.close()
+        leg["peer_handoff"] = hrun
+    except Exception as e:
+        leg["peer_handoff"] = {"error": f"{type(e).__name__}: {e}"}
+    if rank == 0:
+        leg["gpu_vs_reference_parareal"] = reduced_parity(local)
+    return leg
+
+
+def reduced_parity(local):
+    """GPU Parareal(l) against the reference's own parareal::run at reduced size (fixture
+    tests/golden/suspension.npz: 64 x 256, n = 4, 20 RK2 | 2 Euler per interval): max relative
+    position difference over every 4th node of every boundary state (rod_position_metric)."""
+    from paper_2604_12083_b200 import parareal as pr
+    from paper_2604_12083_b200.scenario import ScenarioConfig, build_initial_state, make_scenario
+
+    path = os.path.join(ROOT, "tests", "golden", "suspension.npz")
+    if not os.path.exists(path):
+        return {"error": "tests/golden/suspension.npz missing"}
+    fx = np.load(path)
+    rods, nodes, n, fine, coarse, _, stride = (int(v) for v in fx["meta"])
+    sc = make_scenario(ScenarioConfig(rod_count=rods, nodes_per_rod=nodes, epsilon=float(fx["params"][0])))
+    x0 = build_initial_state(sc)
+    T = n * fine * float(fx["params"][1])
+    out = {"workload": f"{rods} x {nodes}, n={n}, {fine} RK2 | {coarse} Euler per interval, pipelined, tol=1e-300 "
+                       "(the reference ran parareal::run on the CPU; tests/golden/make_suspension.py)"}
+    for l in range(1, n + 1):
+        res = pr.run_gpu(pr.ParallelPlan(horizon=T, intervals=n, workers=n + 1, max_iterations=l, tolerance=1e-300,
+                                         mode=pr.PIPELINED), sc, fine, coarse, x0, device=local)
+        worst = 0.0
+        for i in range(1, n + 1):
+            got = res.states[i].reshape(-1, 12)[::stride, 0:3]
+            want = fx[f"par_m1_l{l}_n{i}_pos"]
+            worst = max(worst, float((np.sqrt(((got - want) ** 2).sum(1)) / np.sqrt((want ** 2).sum(1))).max()))
+        out[f"l{l}"] = worst
+    return out
 
 
 def large_leg(args, local, dev, tr, world, rank):
@@ -549,7 +771,7 @@ def hybrid_leg(args, sc, x0, local, dev, world, members):
     trs = _group_transports(local, groups)
     q, p = rank % members, rank // members
     t_tr, c_tr, f_tr = trs[q], trs[len(tg) + p], trs[len(tg) + len(sg) + p]
-    fine_steps, coarse_steps = args.fine_steps, max(1, args.fine_steps // 10)
+    fine_steps, coarse_steps = args.fine_steps, max(1, min(args.coarse_steps, args.fine_steps // 10))
     plan = pr.ParallelPlan(t0=0.0, horizon=slices * fine_steps * 1e-6, intervals=slices, workers=slices,
                            max_iterations=args.parareal_iters, tolerance=1e-300, mode=pr.PIPELINED)
     try:
@@ -760,14 +982,18 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-targets", type=int, default=4096, help="bounded target sample for the CPU legs")
-    ap.add_argument("--fine-steps", type=int, default=50, help="RK2 steps per interval for the time-step leg")
-    ap.add_argument("--parareal-iters", type=int, default=1)
+    ap.add_argument("--ref-targets", type=int, default=N_POINTS,
+                    help="targets of the CPU legs (default: all, the full N x N evaluation)")
+    ap.add_argument("--fine-steps", type=int, default=1000, help="RK2 steps per interval, N>1 Parareal legs")
+    ap.add_argument("--coarse-steps", type=int, default=100, help="Euler steps per interval, N>1 Parareal legs")
+    ap.add_argument("--serial-steps", type=int, default=200, help="RK2 steps of the N=1 serial fine leg")
+    ap.add_argument("--parareal-iters", type=int, default=1, help="iterations of the hybrid space x time leg")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (profiling runs)")
     ap.add_argument("--no-steps", action="store_true", help="skip the time-step leg")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the N = 64k / 131k MRS points")
     ap.add_argument("--no-large", action="store_true", help="skip the N > 1 large-suspension sweep (configs[4])")
     ap.add_argument("--large-fine-steps", type=int, default=8, help="RK2 steps per interval, large sweep")
-    ap.add_argument("--large-max-iters", type=int, default=3, help="largest Parareal iteration count swept")
+    ap.add_argument("--large-max-iters", type=int, default=4, help="largest Parareal iteration count swept")
     ap.add_argument("--wire", default="nccl", choices=["nccl", "gloo"],
                     help="N>1 transport; gloo = test mode (ranks may share one GPU, staged host transports)")
     args = ap.parse_args()

@@ -261,12 +261,16 @@ typedef struct pswim_report {
 typedef int (*pswim_propagator_fn)(void* user, double t0, double t1, const double* in,
                                    double* out, int64_t len, void* stream);
 
-/* Trace event (schedule_trace.hpp:14-19).  kind: 0 coarse, 1 fine, 2 correct, 3 idle. */
+/* Trace event (schedule_trace.hpp:14-19).  kind: 0 coarse, 1 fine, 2 correct, 3 idle.
+ * iteration / interval: the task's (k, n) in the Parareal grid (-1 for idle gaps), so a
+ * trace shows which iteration's wavefront ran when. */
 typedef struct pswim_trace_event {
     int32_t worker;
     int32_t kind;
     double t_start;
     double t_end;
+    int32_t iteration;
+    int32_t interval;
 } pswim_trace_event;
 
 /* parareal::run (parareal.hpp:85-86, src/parareal.cpp:118-438) over HOST states with
@@ -304,6 +308,12 @@ typedef struct pswim_transport {
     int (*allreduce_max)(void* user, double* buf, int64_t len, void* stream);
     /* recv[r * count + i] = send_of_rank_r[i] for every rank r (rank-major) */
     int (*allgather)(void* user, const double* send, double* recv, int64_t count, void* stream);
+    /* optional (NULL = always healthy): 0 while the transport works, else a PSWIM_E* code
+     * (NCCL: ncclCommGetAsyncError).  The rank drivers poll it while they wait on the device. */
+    int (*health)(void* user);
+    /* optional: abandon every pending operation so waits return (NCCL: ncclCommAbort).  Called
+     * on a failure or on the PSWIM_COMM_TIMEOUT_S timeout (default 900 s). */
+    void (*abort)(void* user);
 } pswim_transport;
 
 /* Device-buffer transport over a host-buffer wire (e.g. a torch.distributed gloo group or a
@@ -313,15 +323,44 @@ typedef struct pswim_transport {
 pswim_transport* pswim_staged_transport_create(const pswim_transport* host_wire, int device);
 void pswim_staged_transport_destroy(pswim_transport* t);
 
+/* Slice hand-off over peer memory (NVLink P2P / CUDA IPC; csrc/handoff.cu): the producing
+ * kernel of rank p -- the corrector, or a push after the coarse sweep / the exact fine solve --
+ * stores X[k][n] straight into rank p+1's receive slot k and releases a system-scope flag;
+ * rank p+1 waits on the flag on its coarse stream and reads the slot in place.  Each rank
+ * creates one on its device with `slots` >= max_iterations + 1 slots of `len` doubles, shares
+ * the IPC handle (64 bytes; or the local base for ranks that are threads of one process) and
+ * connects to rank p+1's (the last rank connects to nothing).  Replaces the ncclSend/ncclRecv
+ * pair of the state hand-off; the transport then carries only the metric allreduce. */
+typedef struct pswim_handoff pswim_handoff;
+pswim_handoff* pswim_handoff_create(int device, int64_t len, int32_t slots);
+int pswim_handoff_handle(pswim_handoff* h, uint8_t* handle64);
+void* pswim_handoff_local_base(pswim_handoff* h);
+int pswim_handoff_connect(pswim_handoff* h, const uint8_t* next_handle64 /* or NULL */,
+                          void* next_local_base /* or NULL */);
+/* Ranks that are threads of one process: the producing kernel still stores into the next
+ * rank's slot, but the arrival is a CUDA event posted under a host lock instead of a
+ * device-side flag spin (streams of one process share its hardware work queues, so a spin
+ * could sit in front of the very store it waits for). */
+int pswim_handoff_connect_local(pswim_handoff* h, pswim_handoff* next);
+void pswim_handoff_destroy(pswim_handoff* h);
+
 /* Rank driver: rank p owns interval p+1 of a plan with intervals == world.  Runs the
  * pipelined (or regular) Parareal recurrence of src/parareal.cpp:58-89 with one state
- * hand-off per iteration to rank p+1 and one allreduce(max) of the iteration metric.
+ * hand-off per iteration to rank p+1 (transport send/recv, or `handoff` when non-NULL) and
+ * one allreduce(max) of the iteration metric.  Whole iterations are enqueued ahead of the
+ * stop decisions (PSWIM_PARAREAL_LOOKAHEAD for tolerance plans; fixed-iteration plans, tol
+ * < 1e-200, decide at the end), so the host never blocks per task.
  * Final boundary state X[k_final][p+1] goes to h_state_out; the report is identical on
- * every rank.  GPU form: fine = RK2, coarse = Euler on the context's device. */
+ * every rank, and so is the schedule trace (every rank's coarse / corrector tasks on worker 0,
+ * rank p's fine solves on worker p+1, device timestamps against a common start barrier,
+ * idle gaps as ScheduleTrace::finalize_idle, schedule_trace.cpp:17-49; report.schedule_idle =
+ * W).  trace_out may be NULL.  GPU form: fine = RK2, coarse = Euler on `device`. */
 int pswim_parareal_rank_gpu(const pswim_plan* plan, const pswim_scenario* sc, int device,
-                            const pswim_transport* tr, int64_t fine_steps, int64_t coarse_steps,
-                            const double* h_x0, const double* h_reference_slice /* or NULL */,
-                            double* h_state_out, pswim_report* report);
+                            const pswim_transport* tr, pswim_handoff* handoff /* or NULL */,
+                            int64_t fine_steps, int64_t coarse_steps, const double* h_x0,
+                            const double* h_reference_slice /* or NULL */, double* h_state_out,
+                            pswim_report* report, pswim_trace_event* trace_out, int64_t trace_cap,
+                            int64_t* trace_len);
 
 /* Hybrid space x time: the rank is member q of the space group of slice
  * p.  time_tr connects the q-th members of all slices (rank = slice, world = intervals) and
@@ -334,7 +373,8 @@ int pswim_parareal_rank_gpu_hybrid(const pswim_plan* plan, const pswim_scenario*
                                    const pswim_transport* space_fine, int64_t fine_steps,
                                    int64_t coarse_steps, const double* h_x0,
                                    const double* h_reference_slice /* or NULL */, double* h_state_out,
-                                   pswim_report* report);
+                                   pswim_report* report, pswim_trace_event* trace_out,
+                                   int64_t trace_cap, int64_t* trace_len);
 
 /* Host form of the same rank driver (host propagators + host transport): used by the
  * world_size>1 CPU tests of the rank logic. */
@@ -342,7 +382,8 @@ int pswim_parareal_rank_host(const pswim_plan* plan, pswim_propagator_fn coarse,
                              pswim_propagator_fn fine, void* fine_user, const pswim_transport* tr,
                              const double* h_x0, int64_t len, int32_t metric_dim,
                              int32_t metric_stride, const double* h_reference_slice,
-                             double* h_state_out, pswim_report* report);
+                             double* h_state_out, pswim_report* report, pswim_trace_event* trace_out,
+                             int64_t trace_cap, int64_t* trace_len);
 
 /* NCCL transport for one process per GPU.  The unique id (128 bytes) is produced by rank 0
  * with pswim_nccl_unique_id and distributed by the caller (e.g. torch.distributed store). */
@@ -388,12 +429,14 @@ int pswim_propagate_sharded_peer(pswim_ctx* ctx, pswim_peer_group* g, const doub
                                  double* d_out);
 
 /* In-process transport: `world` slice ranks as threads of one process, each on its own
- * context (any device mix), hand-offs by stream-ordered peer copies + events. */
+ * context (any device mix), hand-offs by stream-ordered peer copies + events, or (handoff = 1)
+ * by the peer-memory hand-off.  The trace is rank 0's (= every rank's) gathered trace. */
 int pswim_parareal_run_threads(const pswim_plan* plan, const pswim_scenario* sc,
                                const int* devices /* world entries */, int64_t fine_steps,
                                int64_t coarse_steps, const double* h_x0,
                                const double* h_reference, double* h_states_out,
-                               pswim_report* report);
+                               pswim_report* report, int32_t handoff, pswim_trace_event* trace_out,
+                               int64_t trace_cap, int64_t* trace_len);
 
 /* ---- microbenchmarks used by bench.py for the roofline denominators ------------------- */
 /* Measured FP64 FMA throughput (FLOP/s, 2 per DFMA) of a register-resident DFMA loop over

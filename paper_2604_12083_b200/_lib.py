@@ -67,7 +67,8 @@ class Report(C.Structure):
 
 
 class TraceEvent(C.Structure):
-    _fields_ = [("worker", C.c_int32), ("kind", C.c_int32), ("t_start", C.c_double), ("t_end", C.c_double)]
+    _fields_ = [("worker", C.c_int32), ("kind", C.c_int32), ("t_start", C.c_double), ("t_end", C.c_double),
+                ("iteration", C.c_int32), ("interval", C.c_int32)]
 
 
 PROPAGATOR_FN = C.CFUNCTYPE(C.c_int, _vp, C.c_double, C.c_double, _dp, _dp, _i64, _vp)
@@ -75,11 +76,14 @@ SEND_FN = C.CFUNCTYPE(C.c_int, _vp, _dp, _i64, _i32, _vp)
 RECV_FN = C.CFUNCTYPE(C.c_int, _vp, _dp, _i64, _i32, _vp)
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, _vp, _dp, _i64, _vp)
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, _vp, _dp, _dp, _i64, _vp)
+HEALTH_FN = C.CFUNCTYPE(C.c_int, _vp)
+ABORT_FN = C.CFUNCTYPE(None, _vp)
 
 
 class Transport(C.Structure):
     _fields_ = [("user", _vp), ("rank", C.c_int32), ("world", C.c_int32), ("send", SEND_FN),
-                ("recv", RECV_FN), ("allreduce_max", ALLREDUCE_FN), ("allgather", ALLGATHER_FN)]
+                ("recv", RECV_FN), ("allreduce_max", ALLREDUCE_FN), ("allgather", ALLGATHER_FN),
+                ("health", HEALTH_FN), ("abort", ABORT_FN)]
 
 
 # name -> (restype, argtypes); the complete export list of include/pswim_c.h
@@ -121,13 +125,22 @@ SIGNATURES = {
                                           C.POINTER(_i64)]),
     "pswim_parareal_run_gpu": (C.c_int, [C.POINTER(Plan), C.POINTER(Scenario), C.c_int, _i64, _i64, _dp, _dp, _dp,
                                          C.POINTER(Report), C.POINTER(TraceEvent), _i64, C.POINTER(_i64)]),
-    "pswim_parareal_rank_gpu": (C.c_int, [C.POINTER(Plan), C.POINTER(Scenario), C.c_int, C.POINTER(Transport), _i64, _i64,
-                                          _dp, _dp, _dp, C.POINTER(Report)]),
+    "pswim_parareal_rank_gpu": (C.c_int, [C.POINTER(Plan), C.POINTER(Scenario), C.c_int, C.POINTER(Transport), _vp, _i64,
+                                          _i64, _dp, _dp, _dp, C.POINTER(Report), C.POINTER(TraceEvent), _i64,
+                                          C.POINTER(_i64)]),
     "pswim_parareal_rank_gpu_hybrid": (C.c_int, [C.POINTER(Plan), C.POINTER(Scenario), C.c_int, C.POINTER(Transport),
                                                  C.POINTER(Transport), C.POINTER(Transport), _i64, _i64, _dp, _dp,
-                                                 _dp, C.POINTER(Report)]),
+                                                 _dp, C.POINTER(Report), C.POINTER(TraceEvent), _i64,
+                                                 C.POINTER(_i64)]),
     "pswim_parareal_rank_host": (C.c_int, [C.POINTER(Plan), PROPAGATOR_FN, _vp, PROPAGATOR_FN, _vp,
-                                           C.POINTER(Transport), _dp, _i64, _i32, _i32, _dp, _dp, C.POINTER(Report)]),
+                                           C.POINTER(Transport), _dp, _i64, _i32, _i32, _dp, _dp, C.POINTER(Report),
+                                           C.POINTER(TraceEvent), _i64, C.POINTER(_i64)]),
+    "pswim_handoff_create": (_vp, [C.c_int, _i64, _i32]),
+    "pswim_handoff_handle": (C.c_int, [_vp, C.POINTER(C.c_uint8)]),
+    "pswim_handoff_local_base": (_vp, [_vp]),
+    "pswim_handoff_connect": (C.c_int, [_vp, C.POINTER(C.c_uint8), _vp]),
+    "pswim_handoff_connect_local": (C.c_int, [_vp, _vp]),
+    "pswim_handoff_destroy": (None, [_vp]),
     "pswim_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "pswim_nccl_transport_create": (C.POINTER(Transport), [C.POINTER(C.c_uint8), _i32, _i32, C.c_int]),
     "pswim_nccl_transport_destroy": (None, [C.POINTER(Transport)]),
@@ -145,7 +158,8 @@ SIGNATURES = {
     "pswim_propagate_sharded_peer": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_double, C.c_int, _i64, C.c_double,
                                                _vp]),
     "pswim_parareal_run_threads": (C.c_int, [C.POINTER(Plan), C.POINTER(Scenario), C.POINTER(C.c_int), _i64, _i64,
-                                             _dp, _dp, _dp, C.POINTER(Report)]),
+                                             _dp, _dp, _dp, C.POINTER(Report), _i32, C.POINTER(TraceEvent), _i64,
+                                             C.POINTER(_i64)]),
     "pswim_dfma_peak": (C.c_int, [_vp, _dp, _dp]),
     "pswim_dev_fp64_probe": (C.c_int, [_vp, C.c_int, _dp, _dp]),
     "pswim_version": (C.c_char_p, []),

@@ -64,11 +64,11 @@ class Executor {
     virtual ~Executor() = default;
     virtual void reserve(int buffers) = 0;
     virtual void upload(int buf, const double* h) = 0;
-    // out = G or F of `in` over [t0, t1]; kind kCoarse (sweep) or kFine
-    virtual int propagate(int lane, int worker, TaskKind kind, double t0, double t1, int in, int out,
+    // out = G or F of `in` over [t0, t1]; kind kCoarse (sweep) or kFine; (k, n) for the trace
+    virtual int propagate(int lane, int worker, TaskKind kind, int k, int n, double t0, double t1, int in, int out,
                           const std::vector<int>& deps) = 0;
     // gn = G(in) over [t0, t1]; xn = (fp + gn) - go   (one corrector task, kind kCorrect)
-    virtual int correct(int lane, double t0, double t1, int in, int fp, int go, int gn, int xn,
+    virtual int correct(int lane, int k, int n, double t0, double t1, int in, int fp, int go, int gn, int xn,
                         const std::vector<int>& deps) = 0;
     // iteration k's metric row: eta_tilde over `et`, eta over `e`
     virtual void metrics(int lane, int k, const Pairs& et, const Pairs& e, const std::vector<int>& deps) = 0;
@@ -84,20 +84,21 @@ class HostExec final : public Executor {
         : len_(len), c_(c), cu_(cu), f_(f), fu_(fu), dim_(dim), stride_(stride), origin_(Clock::now()) {}
     void reserve(int buffers) override { bufs_.assign(buffers, std::vector<double>(len_)); }
     void upload(int buf, const double* h) override { std::memcpy(bufs_[buf].data(), h, len_ * sizeof(double)); }
-    int propagate(int, int worker, TaskKind kind, double t0, double t1, int in, int out,
+    int propagate(int, int worker, TaskKind kind, int k, int n, double t0, double t1, int in, int out,
                   const std::vector<int>&) override {
         const double a = now();
         call(kind == kFine ? f_ : c_, kind == kFine ? fu_ : cu_, t0, t1, in, out);
-        events_.push_back(pswim_trace_event{worker, kind, a, now()});
+        events_.push_back(pswim_trace_event{worker, kind, a, now(), k, n});
         return -1;
     }
-    int correct(int, double t0, double t1, int in, int fp, int go, int gn, int xn, const std::vector<int>&) override {
+    int correct(int, int k, int n, double t0, double t1, int in, int fp, int go, int gn, int xn,
+                const std::vector<int>&) override {
         const double a = now();
         call(c_, cu_, t0, t1, in, gn);
         const double *p = bufs_[fp].data(), *g = bufs_[gn].data(), *o = bufs_[go].data();
         double* x = bufs_[xn].data();
         for (int64_t i = 0; i < len_; ++i) x[i] = (p[i] + g[i]) - o[i];  // parareal.cpp:52
-        events_.push_back(pswim_trace_event{0, kCorrect, a, now()});
+        events_.push_back(pswim_trace_event{0, kCorrect, a, now(), k, n});
         return -1;
     }
     void metrics(int, int k, const Pairs& et, const Pairs& e, const std::vector<int>&) override {
@@ -197,18 +198,18 @@ class GpuExec final : public Executor {
         cudaStreamSynchronize(lanes_[0]->stream);  // uploads done; pageable sources released
         cudaEventRecord(origin_, lanes_[0]->stream);
     }
-    int propagate(int lane, int worker, TaskKind kind, double t0, double t1, int in, int out,
+    int propagate(int lane, int worker, TaskKind kind, int k, int n, double t0, double t1, int in, int out,
                   const std::vector<int>& deps) override {
-        pswim_ctx* c = begin(lane, deps, worker, kind);
+        pswim_ctx* c = begin(lane, deps, worker, kind, k, n);
         const bool fine = kind == kFine;
         const int rc = c->propagate_async(ptr(in), t0, t1, fine ? PSWIM_RK2 : PSWIM_EULER,
                                           fine ? fine_steps_ : coarse_steps_, 0.0, ptr(out));
         if (rc) throw CodeError(rc, c->err);
         return end(c);
     }
-    int correct(int lane, double t0, double t1, int in, int fp, int go, int gn, int xn,
+    int correct(int lane, int k, int n, double t0, double t1, int in, int fp, int go, int gn, int xn,
                 const std::vector<int>& deps) override {
-        pswim_ctx* c = begin(lane, deps, 0, kCorrect);
+        pswim_ctx* c = begin(lane, deps, 0, kCorrect, k, n);
         const int rc = c->propagate_async(ptr(in), t0, t1, PSWIM_EULER, coarse_steps_, 0.0, ptr(gn));
         if (rc) throw CodeError(rc, c->err);
         if (correct_launch(ptr(fp), ptr(gn), ptr(go), len_, ptr(xn), c->stream) != cudaSuccess)
@@ -268,7 +269,7 @@ class GpuExec final : public Executor {
             float a = 0.f, b = 0.f;
             cudaEventElapsedTime(&a, origin_, t.a);
             cudaEventElapsedTime(&b, origin_, t.b);
-            out->push_back(pswim_trace_event{t.worker, t.kind, 1e-3 * a, 1e-3 * b});
+            out->push_back(pswim_trace_event{t.worker, t.kind, 1e-3 * a, 1e-3 * b, t.k, t.n});
         }
         return finalize_idle(out);
     }
@@ -276,7 +277,7 @@ class GpuExec final : public Executor {
   private:
     struct Task {
         cudaEvent_t a = nullptr, b = nullptr;
-        int32_t worker = 0, kind = 0;
+        int32_t worker = 0, kind = 0, k = 0, n = 0;
     };
     struct Row {
         cudaEvent_t ready = nullptr;
@@ -288,13 +289,15 @@ class GpuExec final : public Executor {
             if (d >= 0 && cudaStreamWaitEvent(c->stream, tasks_[d].b, 0) != cudaSuccess)
                 throw CodeError(PSWIM_ECUDA, "parareal: event wait");
     }
-    pswim_ctx* begin(int lane, const std::vector<int>& deps, int worker, TaskKind kind) {
+    pswim_ctx* begin(int lane, const std::vector<int>& deps, int worker, TaskKind kind, int k, int n) {
         pswim_ctx* c = lanes_[lane];
         c->use();
         wait(c, deps);
         Task t;
         t.worker = worker;
         t.kind = kind;
+        t.k = k;
+        t.n = n;
         if (cudaEventCreate(&t.a) != cudaSuccess || cudaEventCreate(&t.b) != cudaSuccess ||
             cudaEventRecord(t.a, c->stream) != cudaSuccess)
             throw CodeError(PSWIM_ECUDA, "parareal: task event");
@@ -404,7 +407,7 @@ class Wavefront {
     void sweep() {  // iteration 0: X[0][n] = G(X[0][n-1])
         for (int n = 1; n <= N_; ++n) {
             const int out = take();
-            const int mark = ex_.propagate(wave_lane(0), 0, kCoarse, t(n - 1), t(n), X_[0][n - 1].buf, out,
+            const int mark = ex_.propagate(wave_lane(0), 0, kCoarse, 0, n, t(n - 1), t(n), X_[0][n - 1].buf, out,
                                            {X_[0][n - 1].mark});
             G_[0][n] = X_[0][n] = Cell{out, mark};
         }
@@ -415,7 +418,7 @@ class Wavefront {
         std::vector<int> all_fine;
         for (int n = k; n <= N_; ++n) {  // fine_parallel: F(X[k-1][n-1])
             const int out = take();
-            const int mark = ex_.propagate(fine_lane(n), fine_worker(n), kFine, t(n - 1), t(n), X_[k - 1][n - 1].buf,
+            const int mark = ex_.propagate(fine_lane(n), fine_worker(n), kFine, k, n, t(n - 1), t(n), X_[k - 1][n - 1].buf,
                                            out, {X_[k - 1][n - 1].mark});
             F_[k][n] = Cell{out, mark};
             all_fine.push_back(mark);
@@ -428,7 +431,7 @@ class Wavefront {
             deps.push_back(X_[k][n - 1].mark);
             deps.push_back(G_[k - 1][n].mark);
             const int gn = take(), xn = take();
-            const int mark = ex_.correct(wl, t(n - 1), t(n), X_[k][n - 1].buf, F_[k][n].buf, G_[k - 1][n].buf, gn,
+            const int mark = ex_.correct(wl, k, n, t(n - 1), t(n), X_[k][n - 1].buf, F_[k][n].buf, G_[k - 1][n].buf, gn,
                                          xn, deps);
             G_[k][n] = Cell{gn, mark};
             X_[k][n] = Cell{xn, mark};

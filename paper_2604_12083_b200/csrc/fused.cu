@@ -337,19 +337,21 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
     cluster_barrier<CS>();  // no CTA may exit while others still push partials into it
 }
 
+// Function attributes are set once per process, at context creation (fused_preload), never on
+// a launch path: a driver call that takes the context lock while a peer's device-side wait is
+// pending could otherwise stall another thread's launch (Parareal peer hand-offs).
+template <int CS>
+cudaError_t configure_cs() {
+    cudaError_t e = cudaFuncSetAttribute(fused_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess && CS > 8)
+        e = cudaFuncSetAttribute(fused_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return e;
+}
+
 template <int CS>
 cudaError_t launch_cs(const FusedArgs& a, size_t smem, double* state, int64_t steps, double t0, double dt, int scheme,
                       unsigned* flags, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fused_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        if (CS > 8) {
-            e = cudaFuncSetAttribute(fused_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            if (e != cudaSuccess) return e;
-        }
-        configured = true;
-    }
+    // (function attributes: configure_cs, run by fused_preload at context creation)
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(CS);
     cfg.blockDim = dim3(kFusedThreads);
@@ -397,6 +399,15 @@ int fused_cluster_size(const RodParams& p, int max_hint) {
 }
 
 void fused_preload() {
+    static const bool once = [] {
+        configure_cs<1>();
+        configure_cs<2>();
+        configure_cs<4>();
+        configure_cs<8>();
+        configure_cs<16>();
+        return true;
+    }();
+    (void)once;
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, fused_kernel<1>);
     cudaFuncGetAttributes(&a, fused_kernel<2>);

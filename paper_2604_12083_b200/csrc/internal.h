@@ -148,6 +148,15 @@ cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t st
                                    unsigned* flags, cudaStream_t st, unsigned long long* prof = nullptr,
                                    int max_hint = 0);
 
+// ---- slice hand-off over peer memory (handoff.cu) -----------------------------------------
+double* handoff_recv_slot(pswim_handoff* h, int k);  // this rank's slot k (X[k][n-1] arrives here)
+bool handoff_has_next(const pswim_handoff* h);
+unsigned long long handoff_begin_run(pswim_handoff* h);
+cudaError_t handoff_wait_launch(pswim_handoff* h, int k, unsigned long long gen, cudaStream_t st);
+cudaError_t handoff_push_launch(pswim_handoff* h, int k, unsigned long long gen, const double* src, cudaStream_t st);
+cudaError_t handoff_correct_push_launch(pswim_handoff* h, int k, unsigned long long gen, const double* xp,
+                                        const double* gn, const double* go, double* out, cudaStream_t st);
+
 // ---- host scenario (scenario.cpp) -------------------------------------------------------
 int resolve_scenario(const pswim_scenario* sc, pswim_resolved* out, std::string* err);
 RodParams rod_params(const pswim_scenario* sc, const pswim_resolved& rs);

@@ -33,6 +33,8 @@ struct NcclApi {
     decltype(&ncclRecv) recv = nullptr;
     decltype(&ncclAllReduce) all_reduce = nullptr;
     decltype(&ncclAllGather) all_gather = nullptr;
+    decltype(&ncclCommGetAsyncError) async_error = nullptr;  // optional: health polling
+    decltype(&ncclCommAbort) comm_abort = nullptr;
 };
 
 NcclApi& api() {
@@ -51,6 +53,8 @@ NcclApi& api() {
         a.recv = reinterpret_cast<decltype(a.recv)>(dlsym(h, "ncclRecv"));
         a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
         a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+        a.async_error = reinterpret_cast<decltype(a.async_error)>(dlsym(h, "ncclCommGetAsyncError"));
+        a.comm_abort = reinterpret_cast<decltype(a.comm_abort)>(dlsym(h, "ncclCommAbort"));
         a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.send && a.recv && a.all_reduce &&
                a.all_gather;
     });
@@ -61,6 +65,7 @@ struct NcclTransport {
     pswim_transport t;  // first member: the C handle points here
     ncclComm_t comm = nullptr;
     int device = 0;
+    bool aborted = false;
 };
 
 int nc_send(void* u, const double* buf, int64_t len, int32_t peer, void* st) {
@@ -93,6 +98,25 @@ int nc_allgather(void* u, const double* send, double* recv, int64_t count, void*
                             static_cast<cudaStream_t>(st)) == ncclSuccess
                ? PSWIM_OK
                : PSWIM_ECOMM;
+}
+
+// The rank driver polls this while it waits on the device: a peer that died or hit a network
+// error surfaces here instead of as a hang.
+int nc_health(void* u) {
+    auto* n = static_cast<NcclTransport*>(u);
+    if (n->aborted) return PSWIM_ECOMM;
+    if (!api().async_error) return PSWIM_OK;
+    ncclResult_t st = ncclSuccess;
+    if (api().async_error(n->comm, &st) != ncclSuccess) return PSWIM_ECOMM;
+    return (st == ncclSuccess || st == ncclInProgress) ? PSWIM_OK : PSWIM_ECOMM;
+}
+
+void nc_abort(void* u) {
+    auto* n = static_cast<NcclTransport*>(u);
+    if (n->aborted || !n->comm) return;
+    n->aborted = true;
+    if (api().comm_abort) api().comm_abort(n->comm);  // pending kernels return; the comm is gone
+    n->comm = nullptr;
 }
 
 }  // namespace
@@ -130,6 +154,8 @@ pswim_transport* pswim_nccl_transport_create(const uint8_t* id128, int32_t rank,
     n->t.recv = nc_recv;
     n->t.allreduce_max = nc_allreduce;
     n->t.allgather = nc_allgather;
+    n->t.health = nc_health;
+    n->t.abort = nc_abort;
     return &n->t;
 }
 

@@ -69,7 +69,7 @@ inline double finalize_idle(std::vector<pswim_trace_event>* ev) {
             cursor = 0.0;
         }
         if (e.worker != 0 && e.t_start > cursor) {
-            gaps.push_back(pswim_trace_event{e.worker, kIdle, cursor, e.t_start});
+            gaps.push_back(pswim_trace_event{e.worker, kIdle, cursor, e.t_start, -1, -1});
             idle += e.t_start - cursor;
         }
         cursor = std::max(cursor, e.t_end);

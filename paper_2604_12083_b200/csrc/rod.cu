@@ -453,39 +453,47 @@ inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 
 
 // SM count of the current device (persistent grids; results never depend on it).
 inline int num_sms() {
-    int dev = 0, n = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    static const int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
     return n;
+}
+
+// Resident CTAs per SM of a persistent kernel at a given dynamic shared memory size, queried
+// once per (kernel, size) instead of on every launch: launch paths make no driver queries that
+// take the context lock (see fused.cu configure_cs).
+template <typename K>
+int occupancy(K kernel, int block, size_t smem) {
+    static std::mutex mu;
+    static std::vector<std::pair<size_t, int>> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const auto& c : cache)
+        if (c.first == smem) return c.second;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
+    cache.emplace_back(smem, std::max(per_sm, 1));
+    return cache.back().second;
 }
 
 }  // namespace
 
+// (function attributes: set once in rod_preload, at context creation)
 cudaError_t rod_loads_launch(const RodParams& p, const double* state, double t, double* pos, double* f, double* n,
                              double* seg_f, double* seg_n, const double* lj, const double* extra_f,
                              const double* extra_n, unsigned* flags, cudaStream_t st, const double* tdev) {
     const RodArgs a = rod_args(p);
     const size_t smem = sizeof(double) * (size_t)(12 * p.m + 6 * (p.m - 1));
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(rod_loads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = true;
-    }
     const size_t sm = 8 * (size_t)kRodStages * (kTileBytes + 8) + 8 * (size_t)std::max<int64_t>(p.m - 1, 1);
     const bool aligned = (reinterpret_cast<uintptr_t>(state) & 15) == 0;
     if (seg_f == nullptr && aligned && p.rods * p.m < ((int64_t)1 << 30) && sm <= 100 * 1024) {
         // warp-tiled TMA stream (persistent grid, 2 CTAs/SM)
-        static bool wtma_configured = false;
-        if (!wtma_configured) {
-            cudaFuncSetAttribute(rod_loads_wtma_kernel<kRodStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 100 * 1024);
-            wtma_configured = true;
-        }
         const int total = (int)(p.rods * p.m);
         const int tiles = (total + kWarpNodes - 1) / kWarpNodes;
-        int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rod_loads_wtma_kernel<kRodStages>, 256, sm);
-        const int grid = (int)std::min<int64_t>((tiles + 7) / 8, (int64_t)num_sms() * std::max(per_sm, 1));
+        const int per_sm = occupancy(rod_loads_wtma_kernel<kRodStages>, 256, sm);
+        const int grid = (int)std::min<int64_t>((tiles + 7) / 8, (int64_t)num_sms() * per_sm);
         rod_loads_wtma_kernel<kRodStages><<<(unsigned)grid, 256, sm, st>>>(a, total, state, t, tdev, pos, f, n, lj, extra_f,
                                                                            extra_n, flags);
         return cudaGetLastError();
@@ -514,7 +522,18 @@ cudaError_t lj_launch(const RodParams& p, const double* state, double* forces, c
 }
 
 void rod_preload() {
-    // see peer_preload (mrs.cu): load every per-step kernel before peers can spin
+    // see peer_preload (mrs.cu): load every per-step kernel before peers can spin, and set the
+    // function attributes the launch paths would otherwise set on first use
+    static const bool once = [] {
+        cudaFuncSetAttribute(rod_loads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(rod_loads_wtma_kernel<kRodStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        cudaFuncSetAttribute(advance_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kAdvStages * kAdvStageBytes + kAdvStages * sizeof(uint64_t)));
+        cudaFuncSetAttribute(sqrt_wtma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(8 * (size_t)kSqrtWarpStages * (kSqrtWarpChunkBytes + sizeof(uint64_t))));
+        return true;
+    }();
+    (void)once;
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, rod_loads_kernel);
     cudaFuncGetAttributes(&a, rod_loads_wtma_kernel<kRodStages>);
@@ -538,15 +557,9 @@ cudaError_t advance_launch(const RodParams& p, const double* state, const double
         return cudaGetLastError();
     }
     const size_t smem = kAdvStages * kAdvStageBytes + kAdvStages * sizeof(uint64_t);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(advance_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
     const int64_t nchunks = (total + kAdvBlock - 1) / kAdvBlock;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, advance_tma_kernel, kAdvBlock, smem);
-    const int64_t grid = std::min<int64_t>(nchunks, (int64_t)num_sms() * std::max(per_sm, 1));
+    const int per_sm = occupancy(advance_tma_kernel, kAdvBlock, smem);
+    const int64_t grid = std::min<int64_t>(nchunks, (int64_t)num_sms() * per_sm);
     advance_tma_kernel<<<(unsigned)grid, kAdvBlock, smem, st>>>(state, u, w, dt, 10.0 * p.ds, total, out, flags);
     return cudaGetLastError();
 }
@@ -561,15 +574,9 @@ cudaError_t sqrt_batched_launch(const double* r9, int64_t count, double* s9, cud
     // per-warp TMA rings over the whole 32-matrix chunks, plain tail
     const int64_t nw = count / 32;
     const size_t wsmem = 8 * (size_t)kSqrtWarpStages * (kSqrtWarpChunkBytes + sizeof(uint64_t));
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(sqrt_wtma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem);
-        configured = true;
-    }
     if (nw > 0) {
-        int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sqrt_wtma_kernel, 256, wsmem);
-        const int64_t grid = std::min<int64_t>((nw + 7) / 8, (int64_t)num_sms() * std::max(per_sm, 1));
+        const int per_sm = occupancy(sqrt_wtma_kernel, 256, wsmem);
+        const int64_t grid = std::min<int64_t>((nw + 7) / 8, (int64_t)num_sms() * per_sm);
         sqrt_wtma_kernel<<<(unsigned)grid, 256, wsmem, st>>>(r9, nw, s9);
     }
     const int64_t tail = count - 32 * nw;

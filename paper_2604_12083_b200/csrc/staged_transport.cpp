@@ -99,7 +99,8 @@ pswim_transport* pswim_staged_transport_create(const pswim_transport* host_wire,
     if (!s) return nullptr;
     s->wire = *host_wire;
     s->device = device;
-    s->t = pswim_transport{s, host_wire->rank, host_wire->world, st_send, st_recv, st_allreduce, st_allgather};
+    s->t = pswim_transport{s, host_wire->rank, host_wire->world, st_send, st_recv, st_allreduce, st_allgather,
+                           nullptr, nullptr};
     return &s->t;
 }
 

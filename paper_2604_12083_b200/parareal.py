@@ -68,6 +68,8 @@ class TraceEvent:
     kind: int
     t_start: float
     t_end: float
+    iteration: int = -1  # the task's (k, n) in the Parareal grid; -1 for idle gaps
+    interval: int = -1
 
 
 @dataclass
@@ -223,7 +225,7 @@ def run(plan: ParallelPlan, coarse, fine, x0, metric=None, reference: Optional[S
                                    ref.ctypes.data_as(C.POINTER(C.c_double)) if ref is not None else None,
                                    out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep), trace, cap, C.byref(tlen))
     _lib.raise_for(rc, "parareal::run failed")
-    events = [TraceEvent(e.worker, e.kind, e.t_start, e.t_end) for e in trace[: min(tlen.value, cap)]]
+    events = _events(trace, tlen)
     return RunResult([out[i].copy() for i in range(n + 1)], _finish(rep, et, ea, ref is not None),
                      ScheduleTrace(plan.workers, 0, events))
 
@@ -249,14 +251,27 @@ def run_gpu(plan: ParallelPlan, scenario, fine_steps: int, coarse_steps: int, x0
                                   ref.ctypes.data_as(C.POINTER(C.c_double)) if ref is not None else None,
                                   out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep), trace, cap, C.byref(tlen))
     _lib.raise_for(rc, "parareal::run (gpu) failed")
-    events = [TraceEvent(e.worker, e.kind, e.t_start, e.t_end) for e in trace[: min(tlen.value, cap)]]
+    events = _events(trace, tlen)
     return RunResult([out[i].copy() for i in range(n + 1)], _finish(rep, et, ea, ref is not None),
                      ScheduleTrace(plan.workers, 0, events))
 
 
+def _trace_buffers(intervals: int):
+    cap = 8 * (intervals + 2) * (intervals + 2) + 64
+    return (_lib.TraceEvent * cap)(), cap, C.c_int64(0)
+
+
+def _events(trace, tlen) -> List[TraceEvent]:
+    return [TraceEvent(e.worker, e.kind, e.t_start, e.t_end, e.iteration, e.interval)
+            for e in trace[: min(tlen.value, len(trace))]]
+
+
 def run_sliced_threads(plan: ParallelPlan, scenario, fine_steps: int, coarse_steps: int, x0,
-                       devices: Sequence[int], reference: Optional[Sequence[np.ndarray]] = None) -> RunResult:
-    """One slice per rank (intervals == len(devices)), ranks as threads of this process."""
+                       devices: Sequence[int], reference: Optional[Sequence[np.ndarray]] = None,
+                       handoff: bool = False) -> RunResult:
+    """One slice per rank (intervals == len(devices)), ranks as threads of this process.
+    ``handoff``: slice states move by the peer-memory hand-off (the producing kernel stores into
+    the next rank's slot) instead of stream-ordered peer copies."""
     _validate(plan)
     if len(devices) != plan.intervals:
         raise _lib.InvalidArgument(1, "run_sliced_threads: one device entry per interval")
@@ -270,13 +285,17 @@ def run_sliced_threads(plan: ParallelPlan, scenario, fine_steps: int, coarse_ste
     out = np.zeros((n + 1, x0.size))
     rep, et, ea = _report_arrays(n)
     devs = (C.c_int * n)(*[int(d) for d in devices])
+    trace, cap, tlen = _trace_buffers(n)
     rc = L.pswim_parareal_run_threads(C.byref(plan.to_c()), C.byref(sc), devs, int(fine_steps), int(coarse_steps),
                                       x0.ctypes.data_as(C.POINTER(C.c_double)),
                                       ref.ctypes.data_as(C.POINTER(C.c_double)) if ref is not None else None,
-                                      out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep))
+                                      out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep), int(bool(handoff)),
+                                      trace, cap, C.byref(tlen))
     _lib.raise_for(rc, "parareal sliced (threads) failed")
-    return RunResult([out[i].copy() for i in range(n + 1)], _finish(rep, et, ea, ref is not None),
-                     ScheduleTrace(plan.intervals, 0, []))
+    res = RunResult([out[i].copy() for i in range(n + 1)], _finish(rep, et, ea, ref is not None),
+                    ScheduleTrace(n + 1, 0, _events(trace, tlen)))
+    res.schedule_idle = float(rep.schedule_idle)
+    return res
 
 
 # ---- one process per rank ----------------------------------------------------------------------
@@ -296,7 +315,8 @@ class TorchTransport:
         self._recv = _lib.RECV_FN(self._recv_cb)
         self._red = _lib.ALLREDUCE_FN(self._red_cb)
         self._gather = _lib.ALLGATHER_FN(self._gather_cb)
-        self.c = _lib.Transport(None, rank, world, self._send, self._recv, self._red, self._gather)
+        self.c = _lib.Transport(None, rank, world, self._send, self._recv, self._red, self._gather, _lib.HEALTH_FN(),
+                                _lib.ABORT_FN())
 
     def _send_cb(self, user, buf, length, peer, stream):
         import torch
@@ -348,6 +368,8 @@ class TorchTransport:
 class RankResult:
     state: np.ndarray  # X[k_final][rank + 1]
     report: ConvergenceReport
+    trace: Optional[ScheduleTrace] = None  # every rank's tasks (identical on all ranks)
+    schedule_idle: float = 0.0            # W of that trace
 
 
 def run_sliced_rank_host(plan: ParallelPlan, coarse, fine, x0, metric=None, reference_slice=None,
@@ -363,13 +385,15 @@ def run_sliced_rank_host(plan: ParallelPlan, coarse, fine, x0, metric=None, refe
     ref = None if reference_slice is None else np.ascontiguousarray(np.asarray(reference_slice, dtype=np.float64))
     cb_c = _wrap_propagator(coarse)
     cb_f = _wrap_propagator(fine)
+    trace, cap, tlen = _trace_buffers(plan.intervals)
     rc = L.pswim_parareal_rank_host(C.byref(plan.to_c()), cb_c, None, cb_f, None, C.byref(tr.c),
                                     x0.ctypes.data_as(C.POINTER(C.c_double)), x0.size, int(metric.dim),
                                     int(metric.stride),
                                     ref.ctypes.data_as(C.POINTER(C.c_double)) if ref is not None else None,
-                                    out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep))
+                                    out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep), trace, cap, C.byref(tlen))
     _lib.raise_for(rc, "parareal rank driver failed")
-    return RankResult(out, _finish(rep, et, ea, ref is not None))
+    return RankResult(out, _finish(rep, et, ea, ref is not None), ScheduleTrace(plan.intervals + 1, 0, _events(trace, tlen)),
+                      float(rep.schedule_idle))
 
 
 class StagedTransport:
@@ -470,14 +494,42 @@ def hybrid_groups(world: int, members: int):
     return time_groups, space_groups
 
 
+class Handoff:
+    """Peer-memory slice hand-off of this rank (pswim_handoff_*): receive slots in this GPU's
+    HBM, connected to the next rank's slots through a CUDA IPC handle (NVLink P2P).  Built
+    collectively: every rank of the torch.distributed group `group` calls it."""
+
+    def __init__(self, device: int, len_: int, slots: int, group=None):
+        import torch.distributed as dist
+
+        L = _lib.lib()
+        self.lib = L
+        self.h = L.pswim_handoff_create(int(device), int(len_), int(slots))
+        if not self.h:
+            raise _lib.DeviceError(6, "pswim_handoff_create failed")
+        hb = (C.c_uint8 * 64)()
+        _lib.raise_for(L.pswim_handoff_handle(self.h, hb), "pswim_handoff_handle failed")
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(hb), group=group)
+        nxt = (C.c_uint8 * 64)(*handles[rank + 1]) if rank + 1 < world else None
+        _lib.raise_for(L.pswim_handoff_connect(self.h, nxt, None), "pswim_handoff_connect failed")
+
+    def close(self):
+        if self.h:
+            self.lib.pswim_handoff_destroy(self.h)
+            self.h = None
+
+
 def run_sliced_rank(plan: ParallelPlan, scenario, fine_steps: int, coarse_steps: int, x0, device: int,
-                    transport=None, reference_slice=None, space=None) -> RankResult:
+                    transport=None, reference_slice=None, space=None, handoff: Optional[Handoff] = None) -> RankResult:
     """This process's slice of a time-sliced pipelined Parareal run on `device` (NCCL).
 
     ``space=(coarse_transport, fine_transport)``: hybrid space x time -- this rank is one
     member of its slice's space group, and every coarse / fine rhs shards the MRS over that
     group (pswim_parareal_rank_gpu_hybrid); ``transport`` then connects the same-index members
-    of all slices."""
+    of all slices.  ``handoff``: slice states move over peer memory (:class:`Handoff`), the
+    transport carrying only the metric allreduce."""
     _validate(plan)
     L = _lib.lib()
     own = transport is None
@@ -487,19 +539,24 @@ def run_sliced_rank(plan: ParallelPlan, scenario, fine_steps: int, coarse_steps:
     out = np.zeros_like(x0)
     rep, et, ea = _report_arrays(plan.intervals)
     ref = None if reference_slice is None else np.ascontiguousarray(np.asarray(reference_slice, dtype=np.float64))
+    trace, cap, tlen = _trace_buffers(plan.intervals)
     try:
         refp = ref.ctypes.data_as(C.POINTER(C.c_double)) if ref is not None else None
         if space is None:
-            rc = L.pswim_parareal_rank_gpu(C.byref(plan.to_c()), C.byref(sc), int(device), tr, int(fine_steps),
+            rc = L.pswim_parareal_rank_gpu(C.byref(plan.to_c()), C.byref(sc), int(device), tr,
+                                           handoff.h if handoff is not None else None, int(fine_steps),
                                            int(coarse_steps), x0.ctypes.data_as(C.POINTER(C.c_double)), refp,
-                                           out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep))
+                                           out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep), trace, cap,
+                                           C.byref(tlen))
         else:
             rc = L.pswim_parareal_rank_gpu_hybrid(C.byref(plan.to_c()), C.byref(sc), int(device), tr, space[0],
                                                   space[1], int(fine_steps), int(coarse_steps),
                                                   x0.ctypes.data_as(C.POINTER(C.c_double)), refp,
-                                                  out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep))
+                                                  out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep), trace, cap,
+                                                  C.byref(tlen))
     finally:
         if own:
             L.pswim_nccl_transport_destroy(tr)
     _lib.raise_for(rc, "parareal rank driver (gpu) failed")
-    return RankResult(out, _finish(rep, et, ea, ref is not None))
+    return RankResult(out, _finish(rep, et, ea, ref is not None), ScheduleTrace(plan.intervals + 1, 0, _events(trace, tlen)),
+                      float(rep.schedule_idle))

@@ -38,11 +38,19 @@ def test_bench_multirank_gloo_wire(gpu, world):
     ts = d["time_steps"]
     assert "error" not in ts and ts["value"] > 0 and ts["config"]["intervals"] == world, ts
     assert ts["speedup_vs_serial_fine"] > 0
+    sw = ts["iteration_sweep"]
+    assert [x["iterations"] for x in sw] == list(range(1, min(world, 4) + 1)), sw
+    assert all(x["eta_vs_serial_fine"] is not None for x in sw)
+    assert sw[-1]["eta_vs_serial_fine"] <= sw[0]["eta_vs_serial_fine"]
+    assert "error" not in ts["peer_handoff"], ts["peer_handoff"]
+    assert ts["tolerance_run"]["converged"]
+    gp = ts["gpu_vs_reference_parareal"]
+    assert "error" not in gp and all(gp[f"l{l}"] < 1e-10 for l in range(1, 5)), gp
     sp = ts["space_parallel"]
     assert "error" not in sp and sp["value"] > 0, sp
     assert "error" not in sp["fused_peer_allgather"], sp
     lg = ts["large_suspension"]
-    assert "error" not in lg and len(lg["iteration_sweep"]) == min(world, 3), lg
+    assert "error" not in lg and len(lg["iteration_sweep"]) == min(world, 4), lg
     assert all(x["value"] > 0 and x["iterations"] == i + 1 for i, x in enumerate(lg["iteration_sweep"]))
     if world >= 4:
         hy = ts["hybrid_space_time"]

@@ -85,3 +85,121 @@ def test_sliced_threads_tolerance_stop(gpu):
     assert sl.report.converged == eng.report.converged
     for n in range(5):
         assert np.array_equal(sl.states[n], eng.states[n])
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_sliced_threads_handoff_equals_engine(gpu, mode):
+    """Slice states handed off over peer memory (the corrector kernel stores X[k][n] straight
+    into rank p+1's slot and releases a system-scope flag): bitwise equal to the engine, and
+    to the stream-ordered peer-copy transport."""
+    from paper_2604_12083_b200 import parareal as pr
+    from paper_2604_12083_b200.scenario import ScenarioConfig, build_initial_state, make_scenario
+
+    sc = make_scenario(ScenarioConfig(rod_count=2, nodes_per_rod=32, horizon=4e-3, epsilon=0.08))
+    x0 = build_initial_state(sc)
+    for l in (1, 2, 4):
+        plan = pr.ParallelPlan(horizon=4e-3, intervals=4, workers=4, max_iterations=l, tolerance=1e-300, mode=mode)
+        eng = pr.run_gpu(plan, sc, 20, 2, x0)
+        ho = pr.run_sliced_threads(plan, sc, 20, 2, x0, [0, 0, 0, 0], handoff=True)
+        assert ho.report.eta_tilde == eng.report.eta_tilde
+        assert ho.report.iterations_used == l
+        for n in range(5):
+            assert np.array_equal(ho.states[n], eng.states[n]), (l, n)
+
+
+def test_sliced_trace_shows_pipelining(gpu):
+    """Rank-driver schedule trace from device timestamps: every rank's tasks with their (k, n);
+    in pipelined mode iteration k+1's first corrector starts before iteration k's last one
+    ends (the wavefronts overlap), and the fine lanes report idle time W > 0."""
+    from paper_2604_12083_b200 import parareal as pr
+    from paper_2604_12083_b200.scenario import ScenarioConfig, build_initial_state, make_scenario
+
+    sc = make_scenario(ScenarioConfig(rod_count=4, nodes_per_rod=64, horizon=8e-3, epsilon=0.08))
+    x0 = build_initial_state(sc)
+    n = 6
+    plan = pr.ParallelPlan(horizon=8e-3, intervals=n, workers=n, max_iterations=3, tolerance=1e-300,
+                           mode=pr.PIPELINED)
+    for handoff in (False, True):
+        res = pr.run_sliced_threads(plan, sc, 40, 4, x0, [0] * n, handoff=handoff)
+        ev = res.trace.events
+        corr = [e for e in ev if e.kind == pr.CORRECT]
+        fine = [e for e in ev if e.kind == pr.FINE]
+        assert len([e for e in ev if e.kind == pr.COARSE]) == n
+        assert len(corr) == sum(min(i - 1, 3) for i in range(1, n + 1))
+        assert len(fine) == sum(min(i, 3) for i in range(1, n + 1))
+        assert all(e.worker == e.interval for e in fine) and all(e.worker == 0 for e in corr)
+        assert res.schedule_idle > 0.0
+        for k in (1, 2):
+            last_k = max(e.t_end for e in corr if e.iteration == k)
+            first_k1 = min(e.t_start for e in corr if e.iteration == k + 1)
+            assert first_k1 < last_k, (handoff, k, first_k1, last_k)
+
+
+def _handoff_proc(rank, world, port, q):
+    import os
+
+    os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2604_12083_b200 import parareal as pr
+        from paper_2604_12083_b200.scenario import ScenarioConfig, build_initial_state, make_scenario
+
+        sc = make_scenario(ScenarioConfig(rod_count=2, nodes_per_rod=32, horizon=4e-3, epsilon=0.08))
+        x0 = build_initial_state(sc)
+        out = []
+        for mode in (0, 1):
+            for l in (1, world):
+                plan = pr.ParallelPlan(horizon=4e-3, intervals=world, workers=world, max_iterations=l,
+                                       tolerance=1e-300, mode=mode)
+                st = pr.StagedTransport(0)  # the metric allreduce / trace gather over gloo
+                ho = pr.Handoff(0, x0.size, l + 1)
+                dist.barrier()
+                res = pr.run_sliced_rank(plan, sc, 20, 2, x0, 0, transport=st.ptr, handoff=ho)
+                dist.barrier()  # no rank frees its slots while the previous rank may still write
+                ho.close()
+                st.close()
+                out.append((mode, l, res.state.copy(), res.report.eta_tilde))
+        q.put((rank, out))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_handoff_ipc_processes(gpu):
+    """Two processes on one GPU exchanging CUDA IPC handles of their hand-off slots (the
+    one-process-per-GPU layout of an NVSwitch box): every rank's slice state bitwise equal to
+    the engine's, regular and pipelined."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_2604_12083_b200 import parareal as pr
+    from paper_2604_12083_b200.scenario import ScenarioConfig, build_initial_state, make_scenario
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world = 2
+    ps = [ctx.Process(target=_handoff_proc, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted((q.get(timeout=600) for _ in range(world)), key=lambda t: t[0])
+    for p in ps:
+        p.join(timeout=60)
+    sc = make_scenario(ScenarioConfig(rod_count=2, nodes_per_rod=32, horizon=4e-3, epsilon=0.08))
+    x0 = build_initial_state(sc)
+    for rank, out in res:
+        assert isinstance(out, list), out
+        for mode, l, state, et in out:
+            plan = pr.ParallelPlan(horizon=4e-3, intervals=world, workers=world, max_iterations=l,
+                                   tolerance=1e-300, mode=mode)
+            eng = pr.run_gpu(plan, sc, 20, 2, x0)
+            assert et == eng.report.eta_tilde
+            assert np.array_equal(state, eng.states[rank + 1]), (rank, mode, l)

@@ -35,8 +35,11 @@ def _worker(rank, world, port, mode, l, tol, q):
                                mode=mode)
         ref = brute_force(plan, g, f, x0, world)  # exact (k = n) boundaries as the true-error reference
         res = pr.run_sliced_rank_host(plan, g, f, x0, pr.pointwise_metric(3), reference_slice=ref[rank + 1])
+        lanes = {}
+        for e in res.trace.events:
+            lanes[(e.worker, e.kind)] = lanes.get((e.worker, e.kind), 0) + 1
         q.put((rank, res.state.tolist(), res.report.eta_tilde, res.report.eta, res.report.iterations_used,
-               res.report.converged))
+               res.report.converged, lanes, res.schedule_idle))
     finally:
         dist.destroy_process_group()
 
@@ -67,7 +70,7 @@ def test_rank_driver_matches_brute_force(world, mode, l):
     # engine-level reference for the report
     res = pr.run(pr.ParallelPlan(horizon=1.0, intervals=world, workers=2, max_iterations=l, tolerance=1e-300), g, f,
                  x0, pr.pointwise_metric(3))
-    for rank, state, et, eta, iters, conv in out:
+    for rank, state, et, eta, iters, conv, _, _ in out:
         assert np.array_equal(np.array(state), want[rank + 1]), rank
         assert et == res.report.eta_tilde
         assert iters == l
@@ -85,10 +88,31 @@ def test_rank_driver_tolerance_stop():
                                  mode=pr.PIPELINED), g, f, x0, pr.pointwise_metric(3))
     iters = {o[4] for o in out}
     assert iters == {res.report.iterations_used}
-    for rank, state, et, _, _, conv in out:
+    for rank, state, et, _, _, conv, _, _ in out:
         assert et == res.report.eta_tilde
         assert conv == res.report.converged
         assert np.array_equal(np.array(state), res.states[rank + 1])
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_rank_driver_schedule_trace(mode):
+    """The rank driver's schedule trace (ScheduleTrace semantics, schedule_trace.cpp:17-49):
+    gathered from every rank, identical on all ranks; the serial tier (coarse sweep and
+    correctors of every rank) on worker 0, rank p's fine solves on worker p+1; idle gaps only
+    on fine lanes and W > 0 (no fine lane can start before the coarse sweep reaches it)."""
+    world, l = 4, 2
+    out = _run(world, mode, l, 1e-300)
+    lanes0, idle0 = out[0][6], out[0][7]
+    for o in out:
+        assert o[6] == lanes0 and o[7] == idle0
+    COARSE, FINE, CORRECT, IDLE = 0, 1, 2, 3
+    assert lanes0[(0, COARSE)] == world  # one coarse-sweep task per rank
+    assert lanes0[(0, CORRECT)] == sum(min(n - 1, l) for n in range(1, world + 1))
+    for n in range(1, world + 1):
+        assert lanes0[(n, FINE)] == min(n, l)  # F for k = 1..min(n, l)
+        assert lanes0.get((n, IDLE), 0) >= 1
+    assert (0, IDLE) not in lanes0
+    assert idle0 > 0.0
 
 
 def test_hybrid_rank_layout():
