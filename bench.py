@@ -51,6 +51,15 @@ FLOP_PER_PAIR = 103
 WORKLOAD = "MRS all-pairs velocity evaluation, N=16384 regularized points (BASELINE configs[1])"
 
 
+def _jsonable(o):
+    """numpy scalars / arrays in the JSON line as plain numbers / lists."""
+    if isinstance(o, np.generic):
+        return o.item()
+    if isinstance(o, np.ndarray):
+        return o.tolist()
+    raise TypeError(f"not JSON serializable: {type(o).__name__}")
+
+
 class Mt19937_64:
     """std::mt19937_64 (the C++ standard's 64-bit Mersenne Twister), so the bench draws exactly
     the inputs of the reference's own timer (tools/bench_kernels.cpp:46-50)."""
@@ -255,7 +264,7 @@ def run_reference_arm(args) -> None:
                                                                  "OMP team of 1 thread"}},
         "e2e": {"value": value, "unit": "Gpair/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line, default=_jsonable), flush=True)
 
 
 # ------------------------------------------------------------------------------------------
@@ -450,7 +459,7 @@ def run_ours(args) -> None:
             "time_steps": time_steps,
             "hbm_kernels": hbm,
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line, default=_jsonable), flush=True)
     ctx.close()
     if world > 1:
         barrier()
@@ -640,11 +649,11 @@ def parareal_sweep_leg(args, sc, x0, world, rank, local, dev, tr):
         res = pr.run_sliced_rank(p, sc, fine, coarse, x0, local, transport=tr, reference_slice=ref_slice,
                                  handoff=handoff)
         wall = reduce_max(time.perf_counter() - t0, dev)
-        eta = res.report.eta[-1] if res.report.eta else None
+        eta = float(res.report.eta[-1]) if res.report.eta else None
         return res, {"iterations": res.report.iterations_used, "converged": res.report.converged,
                      "value": world * fine / wall, "unit": "steps/s", "wall_s": wall,
                      "speedup_vs_serial_fine": serial_s / wall, "eta_vs_serial_fine": eta,
-                     "within_tolerance_1e-10": eta is not None and eta <= 1e-10,
+                     "within_tolerance_1e-10": bool(eta is not None and eta <= 1e-10),
                      "eta_tilde": res.report.eta_tilde, "schedule_idle_s": res.schedule_idle}
 
     sweep = [timed(plan(l))[1] for l in range(1, min(4, world) + 1)]

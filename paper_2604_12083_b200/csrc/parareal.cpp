@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
@@ -1068,8 +1069,10 @@ int pswim_parareal_run_threads(const pswim_plan* plan, const pswim_scenario* sc,
                         rcs[p] = rank_run(*plan, be, trs[p], hos[p], len, x0,
                                           reference ? reference + len * (p + 1) : nullptr, states_out + len * (p + 1),
                                           &reps[p], p == 0 ? TraceOut{trace_out, trace_cap, trace_len} : TraceOut{});
+                    if (rcs[p] && rcs[p] != PSWIM_ECOMM) std::fprintf(stderr, "pswim: slice rank %d: %s\n", p, be.error().c_str());
                 } catch (const CodeError& e) {
                     rcs[p] = e.code;
+                    std::fprintf(stderr, "pswim: slice rank %d: %s\n", p, e.what());
                 } catch (...) {
                     rcs[p] = PSWIM_ESTATE;
                 }

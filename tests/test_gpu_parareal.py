@@ -114,10 +114,11 @@ def test_sliced_trace_shows_pipelining(gpu):
     from paper_2604_12083_b200 import parareal as pr
     from paper_2604_12083_b200.scenario import ScenarioConfig, build_initial_state, make_scenario
 
-    sc = make_scenario(ScenarioConfig(rod_count=4, nodes_per_rod=64, horizon=8e-3, epsilon=0.08))
-    x0 = build_initial_state(sc)
     n = 6
-    plan = pr.ParallelPlan(horizon=8e-3, intervals=n, workers=n, max_iterations=3, tolerance=1e-300,
+    T = n * 40 * 1e-6  # dt = 1e-6 fine, 1e-5 coarse: stable for 64-node rods at eps = 0.08
+    sc = make_scenario(ScenarioConfig(rod_count=4, nodes_per_rod=64, horizon=T, epsilon=0.08))
+    x0 = build_initial_state(sc)
+    plan = pr.ParallelPlan(horizon=T, intervals=n, workers=n, max_iterations=3, tolerance=1e-300,
                            mode=pr.PIPELINED)
     for handoff in (False, True):
         res = pr.run_sliced_threads(plan, sc, 40, 4, x0, [0] * n, handoff=handoff)

@@ -13,10 +13,10 @@ from paper_2604_12083_b200.scenario import ScenarioConfig, build_initial_state, 
 PHASES = ["front: nodes+stage (+phased)", "front: advance", "front: segments", "mrs_pairs", "reduce+push", "velocity wait", "final advance"]
 
 
-def profile(kw, steps=2000):
+def profile(kw, steps=2000, cluster=1):
     sc = make_scenario(ScenarioConfig(**kw))
     ctx = Context(0, sc)
-    cs = ctx.lib.pswim_set_fused(ctx.handle, 1)
+    cs = ctx.lib.pswim_set_fused(ctx.handle, cluster)
     x = torch.as_tensor(build_initial_state(sc), device="cuda")
     out = torch.empty_like(x)
     cyc = (C.c_uint64 * 7)()
@@ -37,6 +37,27 @@ def profile(kw, steps=2000):
     ctx.close()
 
 
+def plain(kw, steps=20000, cluster=16):
+    """Steps/s of the fused propagate without the phase timer (the bench's configs[0] leg)."""
+    sc = make_scenario(ScenarioConfig(**kw))
+    ctx = Context(0, sc)
+    cs = ctx.lib.pswim_set_fused(ctx.handle, cluster)
+    x = torch.as_tensor(build_initial_state(sc), device="cuda")
+    out = torch.empty_like(x)
+    ctx.check(ctx.lib.pswim_propagate(ctx.handle, dptr(x), 0.0, 1e-5, 1, 10, 0.0, dptr(out)))
+    st = ctx.torch_stream()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    ctx.check(ctx.lib.pswim_propagate(ctx.handle, dptr(x), 0.0, steps * 1e-6, 1, steps, 0.0, dptr(out)))
+    b.record(st)
+    b.synchronize()
+    print(f"{kw}: cluster {cs}: {steps / (a.elapsed_time(b) * 1e-3):.0f} RK2 steps/s (no timer)")
+    ctx.close()
+
+
 if __name__ == "__main__":
+    plain(dict(rod_count=1, nodes_per_rod=100))
+    profile(dict(rod_count=1, nodes_per_rod=100), cluster=16)
     profile(dict(rod_count=1, nodes_per_rod=100))
     profile(dict(rod_count=4, nodes_per_rod=21, placement=1, lj_well_depth=0.01, seed=2))
