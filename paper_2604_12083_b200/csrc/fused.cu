@@ -43,6 +43,7 @@ struct FusedArgs {
     int off_x, off_xm, off_pos, off_f, off_n, off_seg, off_lj, off_rec, off_part, off_vel;
     int off_x2, off_tile;  // second step-start state buffer; per-warp front tiles (32 x 12)
     int off_bar;           // two mbarriers (velocity buffers)
+    int off_om;            // preferred strain per segment index at the coming rhs time (m - 1)
     int part_stride;  // unused (kept for layout clarity)
     unsigned long long* prof;  // kFusedPhases clock64 counters (CTA 0, thread 0), nullptr = off
 };
@@ -104,7 +105,7 @@ __device__ const double* fused_front(const FusedArgs& a, double* sm, const doubl
             const double* xs = vadv ? tile + 12 * (rod * m - base) : src + 12 * rod * m;  // rod's node 0
             double seg[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             if (valid && lane < 31 && k + 1 < m)
-                if (!rod_segment(a.rod, xs, k, t, seg)) fl |= kFlagDegenerate;
+                if (!rod_segment_om(a.rod, xs, k, sm[a.off_om + k], seg)) fl |= kFlagDegenerate;
             double prev[6];
 #pragma unroll
             for (int q = 0; q < 6; ++q) prev[q] = __shfl_up_sync(0xffffffffu, seg[q], 1);
@@ -142,7 +143,7 @@ __device__ const double* fused_front(const FusedArgs& a, double* sm, const doubl
     double* ljf = sm + a.off_lj;
     for (int s = tid; s < nseg; s += bs) {
         const int r = s / (m - 1), k = s % (m - 1);
-        if (!rod_segment(a.rod, xs + 12 * m * r, k, t, seg + 6 * s)) fl |= kFlagDegenerate;
+        if (!rod_segment_om(a.rod, xs + 12 * m * r, k, sm[a.off_om + k], seg + 6 * s)) fl |= kFlagDegenerate;
     }
     for (int i = tid; i < N; i += bs) {
         double fx = 0, fy = 0, fz = 0;
@@ -208,8 +209,16 @@ __device__ __forceinline__ void vel_wait(uint64_t* vbar, uint32_t& phase, int n)
     }
 }
 
+// The preferred strain of every segment index at time t (rod.cpp:29-32) into the CTA's table:
+// `sin` leaves the segment chains of the front pass.  Filled from the top thread down, so the
+// threads without MRS items take it (the same explicit-rounding rod_strain as every kernel).
+__device__ __forceinline__ void strain_table(const FusedArgs& a, double* sm, double t) {
+    for (int k = (int)blockDim.x - 1 - (int)threadIdx.x; k >= 0; k -= (int)blockDim.x)
+        if (k < a.m - 1) sm[a.off_om + k] = rod_strain(a.rod, k, t);
+}
+
 template <int CS>
-__device__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t* vbar, PhaseClock& pc) {
+__device__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t* vbar, double t_next, PhaseClock& pc) {
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n;
     const double* pos = sm + a.off_pos;
     const double2* rec = reinterpret_cast<const double2*>(sm + a.off_rec);
@@ -238,6 +247,8 @@ __device__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t*
 #pragma unroll
         for (int q = 0; q < 6; ++q) lpart[(c * tpc + il) * 6 + q] = out[q];
     }
+    // the next rhs's strain table (this rhs's front pass has read it: barrier at its end)
+    strain_table(a, sm, t_next);
     __syncthreads();
     pc.mark(3);
     // one thread per (target, component): the chunk partials summed in chunk order 0..C-1
@@ -278,6 +289,7 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
         fence_mbar_init();
     }
     uint32_t vphase[2] = {0u, 0u};
+    strain_table(a, sm, t0);
     cluster_barrier<CS>();  // barriers initialised before any CTA pushes into them
     unsigned fl = 0;
     int parity = 0;
@@ -299,7 +311,8 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
         if (vadv) vel_wait<CS>(&vbar[vp], vphase[vp], N);
         pc.mark(5);
         fused_front<CS>(a, sm, vadv ? xb[cur ^ 1] : xb[cur], vadv, h, xb[cur], t, fl, pc);
-        fused_mrs<CS>(a, sm, vel, &vbar[parity], pc);
+        // time of the next rhs: t + dt/2 (RK2 midpoint) or the next step's t (t += dt below)
+        fused_mrs<CS>(a, sm, vel, &vbar[parity], scheme == PSWIM_EULER ? t + dt : t + 0.5 * dt, pc);
         const int p1 = parity;
         parity ^= 1;
         if (scheme == PSWIM_EULER) {
@@ -312,7 +325,7 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
             vel_wait<CS>(&vbar[p1], vphase[p1], N);
             pc.mark(5);
             fused_front<CS>(a, sm, xb[cur], vel, 0.5 * dt, xm, t + 0.5 * dt, fl, pc);
-            fused_mrs<CS>(a, sm, vel2, &vbar[parity], pc);
+            fused_mrs<CS>(a, sm, vel2, &vbar[parity], t + dt, pc);
             vp = parity;
             parity ^= 1;
             vadv = vel2;
@@ -393,7 +406,7 @@ int fused_cluster_size(const RodParams& p, int max_hint) {
     // shared memory: x, xm (12n each), pos/f/n/lj (3n each), seg, rec (18n), local partials
     // (chunks x tpc x 6), velocities (2 x 6n), x2 (12n), front tiles (warps x 32 x 12)
     const int64_t doubles = 24 * n + 12 * n + 6 * p.rods * (p.m - 1) + 18 * n + plan.chunks * tpc * 6 + 12 * n + 16 +
-                            12 * n + ((n + kFrontNodes - 1) / kFrontNodes) * 32 * 12 + 2;
+                            12 * n + ((n + kFrontNodes - 1) / kFrontNodes) * 32 * 12 + 2 + p.m + 1;
     if (doubles * 8 > 220 * 1024) return 0;
     return cs;
 }
@@ -455,6 +468,7 @@ cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t st
     a.off_x2 = take(12 * a.n);
     a.off_tile = take(((a.n + kFrontNodes - 1) / kFrontNodes) * 32 * 12);
     a.off_bar = take(2);
+    a.off_om = take(a.m);
     const size_t smem = (size_t)off * sizeof(double);
     switch (cs) {
         case 1: return launch_cs<1>(a, smem, state, steps, t0, dt, scheme, flags, st);

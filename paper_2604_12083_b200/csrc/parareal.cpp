@@ -189,8 +189,10 @@ class GpuSlice final : public SliceBackend {
         int lo = 0, hi = 0;
         cudaSetDevice(device);
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        cctx_ = pswim_create(device, &sc, hi);  // coarse + corrector: the critical wavefront
-        fctx_ = pswim_create(device, &sc, lo);  // fine solves
+        hi_ = hi;
+        lo_ = lo;
+        cctx_ = pooled_ctx(device, sc, hi);  // coarse + corrector: the critical wavefront
+        fctx_ = pooled_ctx(device, sc, lo);  // fine solves
         if (!cctx_ || !fctx_) throw CodeError(PSWIM_ECUDA, "rank: cannot create contexts");
         cudaStreamCreateWithPriority(&comm_, cudaStreamNonBlocking, hi);
     }
@@ -212,8 +214,14 @@ class GpuSlice final : public SliceBackend {
         if (d_gather_) cudaFree(d_gather_);
         if (origin_) cudaEventDestroy(origin_);
         if (comm_) cudaStreamDestroy(comm_);
-        pswim_destroy(cctx_);
-        pswim_destroy(fctx_);
+        if (cctx_) {
+            pswim_set_graphs(cctx_, 1);  // back to the defaults before it returns to the pool
+            release_ctx(cctx_, hi_);
+        }
+        if (fctx_) {
+            pswim_set_graphs(fctx_, 1);
+            release_ctx(fctx_, lo_);
+        }
     }
     int alloc(int count, int iterations) override {
         cudaSetDevice(device_);
@@ -419,6 +427,7 @@ class GpuSlice final : public SliceBackend {
     double timeout_;
     pswim_ctx* cctx_ = nullptr;
     pswim_ctx* fctx_ = nullptr;
+    int hi_ = 0, lo_ = 0;
     cudaStream_t comm_ = nullptr;
     std::vector<double*> owned_, bufs_;
     double* d_metric_ = nullptr;
@@ -476,7 +485,6 @@ struct TraceOut {
 // speculative blocks every rank issued drain (their hand-offs are matched pairwise).
 int rank_run(const pswim_plan& plan, SliceBackend& be, const pswim_transport& tr, pswim_handoff* ho, int64_t len,
              const double* x0, const double* ref_slice, double* out, pswim_report* rep, const TraceOut& tout) {
-    const auto t_begin = Clock::now();
     const int p = tr.rank, m = tr.world;
     if (plan.intervals != m || p < 0 || p >= m) return PSWIM_EINVAL;
     const int n = p + 1;
@@ -516,6 +524,7 @@ int rank_run(const pswim_plan& plan, SliceBackend& be, const pswim_transport& tr
     // start barrier (one allreduce on the comm queue) -> a common time origin for the trace
     RT(tr.allreduce_max(tr.user, be.metric_slot(K + 1), 2, cs));
     RK(be.origin());
+    const auto t_begin = Clock::now();  // wall time of the run: from the start barrier on
 
     // X[k][n] leaves for rank p+1 (transport path; the peer hand-off is done by the producer)
     auto send_state = [&](int k, int idx) -> int {

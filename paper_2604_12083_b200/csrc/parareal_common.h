@@ -84,4 +84,9 @@ inline double finalize_idle(std::vector<pswim_trace_event>* ev) {
 // exists, before eta_tilde_k is known).  PSWIM_PARAREAL_LOOKAHEAD overrides (>= 1).
 int parareal_lookahead(const pswim_plan& plan);
 
+// Process-wide pool of scenario contexts (engine lanes, slice ranks): creating one allocates
+// HBM workspaces and synchronises, which would dominate short Parareal runs.
+pswim_ctx* pooled_ctx(int device, const pswim_scenario& sc, int prio);
+void release_ctx(pswim_ctx* c, int prio);
+
 }  // namespace pswim
