@@ -39,6 +39,7 @@ def _compile(src: str) -> tuple[str, str]:
     path = os.path.join(CSRC, src)
     deps = [path] + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))]
     deps.append(os.path.join(ROOT, "include", "pswim_c.h"))
+    deps.append(os.path.join(ROOT, "include", "pswim", "device_math.cuh"))
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj, ""
     cmd = [NVCC, *ARCH, *COMMON, "-Xptxas", "-v", "-c", path, "-o", obj]
