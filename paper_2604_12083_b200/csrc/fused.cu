@@ -26,7 +26,7 @@ namespace cg = cooperative_groups;
 namespace pswim {
 namespace {
 
-constexpr int kFusedThreads = 512;
+constexpr int kFusedThreads = 384;  // 12 warps (>= the 9 front warps at N = 256): 168 registers, no spills
 constexpr int kFrontNodes = 30;  // nodes owned per warp in the warp-tiled front pass
 
 struct FusedArgs {
@@ -44,6 +44,7 @@ struct FusedArgs {
     int off_x2, off_tile;  // second step-start state buffer; per-warp front tiles (32 x 12)
     int off_bar;           // two mbarriers (velocity buffers)
     int off_om;            // preferred strain per segment index at the coming rhs time (m - 1)
+    int off_cb;            // MRS chunk bounds (chunks + 1 ints)
     int part_stride;  // unused (kept for layout clarity)
     unsigned long long* prof;  // kFusedPhases clock64 counters (CTA 0, thread 0), nullptr = off
 };
@@ -94,32 +95,34 @@ __device__ const double* fused_front(const FusedArgs& a, double* sm, const doubl
         if (warp < nw) {
             const int base = kFrontNodes * warp - 1, g = base + lane;
             const bool valid = g >= 0 && g < N;
-            double* tile = sm + a.off_tile + warp * 32 * 12;  // slot l = node base + l
+            double* tile = sm + a.off_tile + warp * 32 * 12;  // planes [12][32]: slot l = node base + l
             // origin of the MRS coordinates: node 0 of the rhs state (advance_node's position
             // update, same operations)
-            const d3 o = vadv ? ld3(src) + ld3(vadv) * h : ld3(src);
-            if (valid && vadv) fl |= advance_node(src + 12 * g, vadv + 6 * g, vadv + 6 * g + 3, h, a.max_disp, tile + 12 * lane);
+            const d3 o = vadv ? ld3s(src, N) + ld3s(vadv, N) * h : ld3s(src, N);
+            // owner lanes (1..30) also write the advanced node into the state buffer dst
+            if (valid && vadv)
+                fl |= advance_node(src + g, vadv + g, vadv + 3 * N + g, h, a.max_disp, tile + lane, N, N, 32,
+                                   lane >= 1 && lane <= kFrontNodes ? dst + g : nullptr, N);
             __syncwarp();
             pc.mark(1);
             const int rod = valid ? (int)__umulhi((unsigned)g, a.m_magic) : 0, k = valid ? g - rod * m : 0;
-            const double* xs = vadv ? tile + 12 * (rod * m - base) : src + 12 * rod * m;  // rod's node 0
+            // the rod's node 0 and the plane stride (tile or state)
+            const double* xs = vadv ? tile + (rod * m - base) : src + rod * m;
+            const int xc = vadv ? 32 : N;
             double seg[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             if (valid && lane < 31 && k + 1 < m)
-                if (!rod_segment_om(a.rod, xs, k, sm[a.off_om + k], seg)) fl |= kFlagDegenerate;
+                if (!rod_segment_om(a.rod, xs, k, sm[a.off_om + k], seg, xc)) fl |= kFlagDegenerate;
             double prev[6];
 #pragma unroll
             for (int q = 0; q < 6; ++q) prev[q] = __shfl_up_sync(0xffffffffu, seg[q], 1);
             pc.mark(2);
             if (valid && lane >= 1 && lane <= kFrontNodes) {
-                const d3 xk = ld3(xs + 12 * k);
-                const d3 xnext = k + 1 < m ? ld3(xs + 12 * (k + 1)) : xk;
-                const d3 xprev = k > 0 ? ld3(xs + 12 * (k - 1)) : xk;
-                if (vadv)
-#pragma unroll
-                    for (int q = 0; q < 12; ++q) dst[12 * g + q] = xs[12 * k + q];
+                const d3 xk = ld3s(xs + k, xc);
+                const d3 xnext = k + 1 < m ? ld3s(xs + k + 1, xc) : xk;
+                const d3 xprev = k > 0 ? ld3s(xs + k - 1, xc) : xk;
                 d3 f, tq;
                 node_loads(a.rod, k, seg, prev, xprev, xk, xnext, f, tq);
-                st3(pos + 3 * g, xk);
+                st3s(pos + g, N, xk);
                 double2 r[9];
                 if (!mrs_stage(&xk.x, 3, &f.x, &tq.x, 0, o.x, o.y, o.z, a.mc.scale, r)) fl |= kFlagNonFinite;
 #pragma unroll
@@ -133,7 +136,7 @@ __device__ const double* fused_front(const FusedArgs& a, double* sm, const doubl
     // phased (LJ) version
     if (vadv) {
         for (int i = tid; i < N; i += bs)
-            fl |= advance_node(src + 12 * i, vadv + 6 * i, vadv + 6 * i + 3, h, a.max_disp, dst + 12 * i);
+            fl |= advance_node(src + i, vadv + i, vadv + 3 * N + i, h, a.max_disp, dst + i, N, N, N);
         __syncthreads();
     }
     const double* xs = vadv ? dst : src;
@@ -143,15 +146,15 @@ __device__ const double* fused_front(const FusedArgs& a, double* sm, const doubl
     double* ljf = sm + a.off_lj;
     for (int s = tid; s < nseg; s += bs) {
         const int r = s / (m - 1), k = s % (m - 1);
-        if (!rod_segment_om(a.rod, xs + 12 * m * r, k, sm[a.off_om + k], seg + 6 * s)) fl |= kFlagDegenerate;
+        if (!rod_segment_om(a.rod, xs + m * r, k, sm[a.off_om + k], seg + 6 * s, N)) fl |= kFlagDegenerate;
     }
     for (int i = tid; i < N; i += bs) {
         double fx = 0, fy = 0, fz = 0;
-        const double xi = xs[12 * i], yi = xs[12 * i + 1], zi = xs[12 * i + 2];
+        const double xi = xs[i], yi = xs[N + i], zi = xs[2 * N + i];
         const int ri = i / m, ki = i - ri * m;
         for (int rj = 0, j = 0; rj < a.lj.rods; ++rj)
             for (int kj = 0; kj < m; ++kj, ++j)
-                lj_pair(a.lj, ri, ki, rj, kj, xi - xs[12 * j], yi - xs[12 * j + 1], zi - xs[12 * j + 2], fx, fy, fz);
+                lj_pair(a.lj, ri, ki, rj, kj, xi - xs[j], yi - xs[N + j], zi - xs[2 * N + j], fx, fy, fz);
         ljf[3 * i] = fx;
         ljf[3 * i + 1] = fy;
         ljf[3 * i + 2] = fz;
@@ -160,18 +163,19 @@ __device__ const double* fused_front(const FusedArgs& a, double* sm, const doubl
     for (int g = tid; g < N; g += bs) {
         const int r = g / m, k = g % m;
         d3 f, tq;
-        rod_node(a.rod, xs + 12 * m * r, seg + 6 * (m - 1) * r, k, f, tq);
+        rod_node(a.rod, xs + m * r, seg + 6 * (m - 1) * r, k, f, tq, N);
         f = f + ld3(ljf + 3 * g) * a.rod.inv_ds;
-        st3(pos + 3 * g, ld3(xs + 12 * g));
+        st3s(pos + g, N, ld3s(xs + g, N));
         st3(fo + 3 * g, f);
         st3(no + 3 * g, tq);
     }
     __syncthreads();
     // stage every source relative to node 0 (the single target block's origin in mrs.cu)
-    const double ox = pos[0], oy = pos[1], oz = pos[2];
+    const double ox = pos[0], oy = pos[N], oz = pos[2 * N];
     for (int j = tid; j < N; j += bs) {
         double2 r[9];
-        if (!mrs_stage(pos, 3, fo, no, j, ox, oy, oz, a.mc.scale, r)) fl |= kFlagNonFinite;
+        const d3 pj = ld3s(pos + j, N);
+        if (!mrs_stage(&pj.x, 0, fo, no, j, ox, oy, oz, a.mc.scale, r)) fl |= kFlagNonFinite;
 #pragma unroll
         for (int q = 0; q < 9; ++q) rec[q * N + j] = r[q];
     }
@@ -217,24 +221,31 @@ __device__ __forceinline__ void strain_table(const FusedArgs& a, double* sm, dou
         if (k < a.m - 1) sm[a.off_om + k] = rod_strain(a.rod, k, t);
 }
 
+// This CTA's MRS targets [i0, i0 + nloc) of the cluster split (tpc per CTA), fixed for the
+// launch: computed once, not per rhs (the divisions sat on every rhs's MRS path).
+struct MrsSplit {
+    int i0, nloc, tpc;
+    unsigned nloc_magic;  // __umulhi(w, nloc_magic) == w / nloc for w < 2^16
+    const int* cb;        // chunk bounds j0(c) = c N / C, c = 0..C (shared memory)
+};
+
 template <int CS>
-__device__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t* vbar, double t_next, PhaseClock& pc) {
+__device__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t* vbar, double t_next, PhaseClock& pc,
+                          const MrsSplit& sp) {
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n;
     const double* pos = sm + a.off_pos;
     const double2* rec = reinterpret_cast<const double2*>(sm + a.off_rec);
-    const double ox = pos[0], oy = pos[1], oz = pos[2];
+    const double ox = pos[0], oy = pos[N], oz = pos[2 * N];
     // MRS: this CTA owns targets [i0, i1); items (target, source chunk) computed here, the
     // chunk partials reduced locally in fixed order (mrs.cu's last-CTA reduction), and each
     // target's 6 velocities pushed to every CTA of the cluster through DSMEM.
-    const int rank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
-    const int tpc = (N + CS - 1) / CS;
-    const int i0 = rank * tpc, i1 = min(N, i0 + tpc), nloc = max(0, i1 - i0);
-    double* lpart = sm + a.off_part;  // [chunks][tpc][6]
-    const unsigned nloc_magic = nloc > 0 ? 0xFFFFFFFFu / (unsigned)nloc + 1u : 0u;  // w / nloc, w < 2^16
+    const int tpc = sp.tpc, i0 = sp.i0, nloc = sp.nloc;
+    double* lpart = sm + a.off_part;  // [chunks][6][tpc]
+    const unsigned nloc_magic = sp.nloc_magic;
     for (int w = tid; w < nloc * a.chunks; w += bs) {
         const int c = (int)__umulhi((unsigned)w, nloc_magic), il = w - c * nloc, i = i0 + il;
-        const int j0 = c * N / a.chunks, j1 = (c + 1) * N / a.chunks;  // (N <= 256: no overflow)
-        const double tx = pos[3 * i] - ox, ty = pos[3 * i + 1] - oy, tz = pos[3 * i + 2] - oz;
+        const int j0 = sp.cb[c], j1 = sp.cb[c + 1];
+        const double tx = pos[i] - ox, ty = pos[N + i] - oy, tz = pos[2 * N + i] - oz;
         MrsAcc acc;
         acc.zero();
 #pragma unroll 2
@@ -245,7 +256,7 @@ __device__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t*
         double out[6];
         mrs_finish(acc, tx, ty, tz, out);
 #pragma unroll
-        for (int q = 0; q < 6; ++q) lpart[(c * tpc + il) * 6 + q] = out[q];
+        for (int q = 0; q < 6; ++q) lpart[(c * 6 + q) * tpc + il] = out[q];  // [chunk][component][target]
     }
     // the next rhs's strain table (this rhs's front pass has read it: barrier at its end)
     strain_table(a, sm, t_next);
@@ -254,19 +265,19 @@ __device__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t*
     // one thread per (target, component): the chunk partials summed in chunk order 0..C-1
     // (mrs.cu's last-CTA reduction, bitwise), then pushed to every CTA of the cluster
     for (int w = tid; w < nloc * 6; w += bs) {
-        const int il = w / 6, q = w - 6 * il;
-        double sum = lpart[w];
+        const int q = (int)__umulhi((unsigned)w, nloc_magic), il = w - q * nloc;  // lane-consecutive targets
+        double sum = lpart[q * tpc + il];
 #pragma unroll 8
-        for (int c = 1; c < a.chunks; ++c) sum += lpart[(c * tpc + il) * 6 + q];
+        for (int c = 1; c < a.chunks; ++c) sum += lpart[(c * 6 + q) * tpc + il];
         const int i = i0 + il;
         if constexpr (CS > 1) {
             // st.async into every CTA (itself included), completion counted on its mbarrier:
             // no cluster barrier and no GPU-scope fence per rhs
-            const uint32_t laddr = smem_u32(vel + 6 * i + q), lbar = smem_u32(vbar);
+            const uint32_t laddr = smem_u32(vel + q * N + i), lbar = smem_u32(vbar);
 #pragma unroll
             for (int rr = 0; rr < CS; ++rr) st_async_f64(cluster_addr(laddr, rr), sum, cluster_addr(lbar, rr));
         } else {
-            vel[6 * i + q] = sum;
+            vel[q * N + i] = sum;
         }
     }
     if (a.prof) __syncthreads();  // phase timer only: end of the push as one CTA-wide instant
@@ -281,7 +292,8 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n;
     double* x = sm + a.off_x;
     double* xm = sm + a.off_xm;
-    for (int k = tid; k < 12 * N; k += bs) x[k] = state[k];
+    // shared-memory state: component planes [12][N] (lane-consecutive nodes, no bank conflicts)
+    for (int k = tid; k < 12 * N; k += bs) x[(k % 12) * N + k / 12] = state[k];
     uint64_t* vbar = reinterpret_cast<uint64_t*>(sm + a.off_bar);  // one mbarrier per velocity buffer
     if (tid == 0) {
         mbar_init(&vbar[0], 1);
@@ -290,6 +302,17 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
     }
     uint32_t vphase[2] = {0u, 0u};
     strain_table(a, sm, t0);
+    MrsSplit sp;
+    {
+        const int rank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
+        sp.tpc = (N + CS - 1) / CS;
+        sp.i0 = rank * sp.tpc;
+        sp.nloc = max(0, min(N, sp.i0 + sp.tpc) - sp.i0);
+        sp.nloc_magic = sp.nloc > 0 ? 0xFFFFFFFFu / (unsigned)sp.nloc + 1u : 0u;
+        int* cb = reinterpret_cast<int*>(sm + a.off_cb);
+        for (int c = tid; c <= a.chunks; c += bs) cb[c] = c * N / a.chunks;  // (N <= 256: no overflow)
+        sp.cb = cb;
+    }
     cluster_barrier<CS>();  // barriers initialised before any CTA pushes into them
     unsigned fl = 0;
     int parity = 0;
@@ -312,7 +335,7 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
         pc.mark(5);
         fused_front<CS>(a, sm, vadv ? xb[cur ^ 1] : xb[cur], vadv, h, xb[cur], t, fl, pc);
         // time of the next rhs: t + dt/2 (RK2 midpoint) or the next step's t (t += dt below)
-        fused_mrs<CS>(a, sm, vel, &vbar[parity], scheme == PSWIM_EULER ? t + dt : t + 0.5 * dt, pc);
+        fused_mrs<CS>(a, sm, vel, &vbar[parity], scheme == PSWIM_EULER ? t + dt : t + 0.5 * dt, pc, sp);
         const int p1 = parity;
         parity ^= 1;
         if (scheme == PSWIM_EULER) {
@@ -325,7 +348,7 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
             vel_wait<CS>(&vbar[p1], vphase[p1], N);
             pc.mark(5);
             fused_front<CS>(a, sm, xb[cur], vel, 0.5 * dt, xm, t + 0.5 * dt, fl, pc);
-            fused_mrs<CS>(a, sm, vel2, &vbar[parity], t + dt, pc);
+            fused_mrs<CS>(a, sm, vel2, &vbar[parity], t + dt, pc, sp);
             vp = parity;
             parity ^= 1;
             vadv = vel2;
@@ -340,12 +363,12 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
         vel_wait<CS>(&vbar[vp], vphase[vp], N);
         pc.mark(5);
         for (int i = tid; i < N; i += bs)
-            fl |= advance_node(xb[cur ^ 1] + 12 * i, vadv + 6 * i, vadv + 6 * i + 3, h, a.max_disp, out + 12 * i);
+            fl |= advance_node(xb[cur ^ 1] + i, vadv + i, vadv + 3 * N + i, h, a.max_disp, out + i, N, N, N);
         __syncthreads();
         pc.mark(6);
     }
     if (crank == 0)
-        for (int k = tid; k < 12 * N; k += bs) state[k] = out[k];
+        for (int k = tid; k < 12 * N; k += bs) state[k] = out[(k % 12) * N + k / 12];
     if (fl) atomicOr(flags, fl);
     cluster_barrier<CS>();  // no CTA may exit while others still push partials into it
 }
@@ -406,7 +429,8 @@ int fused_cluster_size(const RodParams& p, int max_hint) {
     // shared memory: x, xm (12n each), pos/f/n/lj (3n each), seg, rec (18n), local partials
     // (chunks x tpc x 6), velocities (2 x 6n), x2 (12n), front tiles (warps x 32 x 12)
     const int64_t doubles = 24 * n + 12 * n + 6 * p.rods * (p.m - 1) + 18 * n + plan.chunks * tpc * 6 + 12 * n + 16 +
-                            12 * n + ((n + kFrontNodes - 1) / kFrontNodes) * 32 * 12 + 2 + p.m + 1;
+                            12 * n + ((n + kFrontNodes - 1) / kFrontNodes) * 32 * 12 + 2 + p.m + 1 +
+                            (plan.chunks + 2) / 2 + 1;
     if (doubles * 8 > 220 * 1024) return 0;
     return cs;
 }
@@ -469,6 +493,7 @@ cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t st
     a.off_tile = take(((a.n + kFrontNodes - 1) / kFrontNodes) * 32 * 12);
     a.off_bar = take(2);
     a.off_om = take(a.m);
+    a.off_cb = take((plan.chunks + 2) / 2);
     const size_t smem = (size_t)off * sizeof(double);
     switch (cs) {
         case 1: return launch_cs<1>(a, smem, state, steps, t0, dt, scheme, flags, st);
