@@ -872,15 +872,18 @@ def flagellum_leg(args, local, dev):
     st = ctx.torch_stream()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
-    a.record(st)
-    ctx.check(L.pswim_propagate(ctx.handle, dptr(dx), 0.0, steps * 1e-6, 1, steps, 0.0, dptr(out)))
-    b.record(st)
-    b.synchronize()
+    with ClockSampler(local) as fclk:
+        a.record(st)
+        ctx.check(L.pswim_propagate(ctx.handle, dptr(dx), 0.0, steps * 1e-6, 1, steps, 0.0, dptr(out)))
+        b.record(st)
+        b.synchronize()
     gpu = steps / (a.elapsed_time(b) * 1e-3)
-    ctx.close()
     leg = {"metric": "simulated RK2 time-steps/s", "value": gpu, "unit": "steps/s",
            "config": {"workload": "single flagellum, 1 x 100 nodes, serial fine RK2, dt=1e-6 (BASELINE configs[0])",
-                      "steps": steps, "kernel": f"fused propagate, cluster of {cs} CTAs, 1 launch per interval"}}
+                      "steps": steps, "kernel": f"fused propagate, cluster of {cs} CTAs, 1 launch per interval"},
+           "clocks": fclk.summary()}
+    leg["latency_roofline"] = latency_roofline(ctx, sc, cs, gpu, fclk.summary())
+    ctx.close()
     leg["parareal_1gpu"] = parareal_1gpu_leg(sc, x0, local)
     if not args.no_cpu:
         from oracle.pyoracle import LIB_PATHS, Oracle, Scenario as OS
@@ -889,12 +892,50 @@ def flagellum_leg(args, local, dev):
             ref = Oracle("ref")
             osc = OS.make(**kw)
             csteps = 2000
-            t0 = time.perf_counter()
-            ref.propagate(osc, x0, 0.0, csteps * 1e-6, 1, steps=csteps)
-            cpu = csteps / (time.perf_counter() - t0)
-            leg["cpu_baseline"] = {"value": cpu, "unit": "steps/s", "cores": ref.max_threads_(), "kind": "reference",
-                                   "sample": f"{csteps} RK2 steps of the same flagellum (reference propagate, OpenMP)"}
+            full = ref.max_threads_()
+            rates = {}
+            for threads in (full, 1):  # BASELINE §3: the OpenMP team and one thread (the faster one counts)
+                ref.set_threads_(threads)
+                t0 = time.perf_counter()
+                ref.propagate(osc, x0, 0.0, csteps * 1e-6, 1, steps=csteps)
+                rates[threads] = csteps / (time.perf_counter() - t0)
+            ref.set_threads_(full)
+            best = max(rates, key=rates.get)
+            leg["cpu_baseline"] = {"value": rates[best], "unit": "steps/s", "cores": best, "kind": "reference",
+                                   "sample": f"{csteps} RK2 steps of the same flagellum (reference propagate; best of "
+                                             f"the {full}-thread OpenMP team and 1 thread)",
+                                   "by_threads": {str(k): v for k, v in rates.items()}, "nproc": os.cpu_count()}
     return leg
+
+
+def latency_roofline(ctx, sc, cs, steps_per_s, clocks):
+    """Latency roofline of the fused small-system kernel: the per-rhs phases'
+    floors measured live on this GPU by pswim_dev_latency_probe, each phase alone on an idle
+    SM with the kernel's own decomposition -- the front-pass chain on one warp per SMSP, the
+    MRS items (warps x sources per item), the in-order chunk reduction, the 16-CTA velocity
+    exchange -- summed over the two rhs of an RK2 step, against the measured cycles per step."""
+    import ctypes as C
+
+    import math
+
+    n = sc.total_nodes
+    chunks = max(1, (n + 3) // 4)  # mrs_plan's single-block small-system plan
+    tpc = (n + cs - 1) // cs
+    warps = math.ceil(tpc * chunks / 32)
+    ns = math.ceil(n / chunks)
+    out = (C.c_double * 4)()
+    rc = ctx.lib.pswim_dev_latency_probe(ctx.handle, ns, min(warps, 12), chunks, 6 * tpc, 6 * n, out)
+    if rc != 0:
+        return {"error": f"pswim_dev_latency_probe rc={rc}"}
+    floor_rhs = sum(out)
+    mhz = clocks.get("sm_mhz") or 1965.0
+    measured = mhz * 1e6 / steps_per_s
+    return {"bound": "latency", "unit": "cycles/RK2 step", "floor": 2 * floor_rhs, "measured": measured,
+            "frac": 2 * floor_rhs / measured,
+            "floor_per_rhs": {"front_chain": out[0], f"mrs_items_{warps}w_x_{ns}src": out[1],
+                              f"chunk_reduction_{chunks}": out[2], f"exchange_cluster{cs}": out[3]},
+            "note": "each phase timed alone on an idle SM (clock64, pswim_dev_latency_probe); measured = "
+                    "SM clock / steps per s"}
 
 
 def parareal_1gpu_leg(sc, x0, local, n=8, fine=1000, coarse=100):

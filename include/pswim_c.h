@@ -447,6 +447,11 @@ int pswim_dfma_peak(pswim_ctx* ctx, double* flops_per_s, double* ms);
  * register operands, 2 three distinct register pairs per DFMA, 3 DMUL, 4 kind 2 + MUFU.RSQ64H);
  * returns FP64 instructions per second (one lane-op each). */
 int pswim_dev_fp64_probe(pswim_ctx* ctx, int kind, double* ops_per_s, double* ms);
+/* Latency floors of the fused small-system kernel's per-rhs phases on this GPU, cycles each:
+ * out4[0] front-pass chain (one warp per SMSP), out4[1] MRS items (ns sources per item, `warps`
+ * warps), out4[2] the in-order reduction of `chunks` partials, out4[3] the velocity exchange of a
+ * 16-CTA cluster (per_cta values per CTA, total over the cluster).  Dev diagnostics. */
+int pswim_dev_latency_probe(pswim_ctx* ctx, int ns, int warps, int chunks, int per_cta, int total, double* out4);
 
 /* Library version string. */
 const char* pswim_version(void);

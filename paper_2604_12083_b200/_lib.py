@@ -162,6 +162,7 @@ SIGNATURES = {
                                              C.POINTER(_i64)]),
     "pswim_dfma_peak": (C.c_int, [_vp, _dp, _dp]),
     "pswim_dev_fp64_probe": (C.c_int, [_vp, C.c_int, _dp, _dp]),
+    "pswim_dev_latency_probe": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp]),
     "pswim_version": (C.c_char_p, []),
 }
 

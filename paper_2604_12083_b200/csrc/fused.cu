@@ -28,6 +28,9 @@ namespace {
 
 constexpr int kFusedThreads = 384;  // 12 warps (>= the 9 front warps at N = 256): 168 registers, no spills
 constexpr int kFrontNodes = 30;  // nodes owned per warp in the warp-tiled front pass
+// KP (template): plane stride of the shared-memory state, velocity, position and source-record
+// planes, 128 or 256 (>= n): a compile-time constant, so every strided access in the per-node
+// chains folds into an immediate offset instead of integer address arithmetic.
 
 struct FusedArgs {
     RodArgs rod;
@@ -84,8 +87,8 @@ __device__ __forceinline__ void cluster_barrier() {
 // advances them into a per-warp tile, computes segment (g, g+1) per lane and gets segment
 // g - 1 by one shuffle -- the layout of rod_loads_wtma_kernel.  LJ needs every advanced
 // position first, so LJ systems take the phased version.
-template <int CS>
-__device__ const double* fused_front(const FusedArgs& a, double* sm, const double* src, const double* vadv, double h,
+template <int CS, int KP>
+__device__ __forceinline__ const double* fused_front(const FusedArgs& a, double* sm, const double* src, const double* vadv, double h,
                                      double* dst, double t, unsigned& fl, PhaseClock& pc) {
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n, m = a.m, nseg = a.rods * (m - 1);
     double* pos = sm + a.off_pos;
@@ -98,17 +101,21 @@ __device__ const double* fused_front(const FusedArgs& a, double* sm, const doubl
             double* tile = sm + a.off_tile + warp * 32 * 12;  // planes [12][32]: slot l = node base + l
             // origin of the MRS coordinates: node 0 of the rhs state (advance_node's position
             // update, same operations)
-            const d3 o = vadv ? ld3s(src, N) + ld3s(vadv, N) * h : ld3s(src, N);
-            // owner lanes (1..30) also write the advanced node into the state buffer dst
+            const d3 o = vadv ? ld3s(src, KP) + ld3s(vadv, KP) * h : ld3s(src, KP);
+            // the rhs state's node into the warp tile: advanced from src (owner lanes 1..30 also
+            // write it into the state buffer dst), or src's node itself for the first rhs
             if (valid && vadv)
-                fl |= advance_node(src + g, vadv + g, vadv + 3 * N + g, h, a.max_disp, tile + lane, N, N, 32,
-                                   lane >= 1 && lane <= kFrontNodes ? dst + g : nullptr, N);
+                fl |= advance_node(src + g, vadv + g, vadv + 3 * KP + g, h, a.max_disp, tile + lane, KP, KP, 32,
+                                   lane >= 1 && lane <= kFrontNodes ? dst + g : nullptr, KP);
+            else if (valid)
+#pragma unroll
+                for (int q = 0; q < 12; ++q) tile[q * 32 + lane] = src[q * KP + g];
             __syncwarp();
             pc.mark(1);
             const int rod = valid ? (int)__umulhi((unsigned)g, a.m_magic) : 0, k = valid ? g - rod * m : 0;
             // the rod's node 0 and the plane stride (tile or state)
-            const double* xs = vadv ? tile + (rod * m - base) : src + rod * m;
-            const int xc = vadv ? 32 : N;
+            const double* xs = tile + (rod * m - base);
+            constexpr int xc = 32;
             double seg[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             if (valid && lane < 31 && k + 1 < m)
                 if (!rod_segment_om(a.rod, xs, k, sm[a.off_om + k], seg, xc)) fl |= kFlagDegenerate;
@@ -122,11 +129,11 @@ __device__ const double* fused_front(const FusedArgs& a, double* sm, const doubl
                 const d3 xprev = k > 0 ? ld3s(xs + k - 1, xc) : xk;
                 d3 f, tq;
                 node_loads(a.rod, k, seg, prev, xprev, xk, xnext, f, tq);
-                st3s(pos + g, N, xk);
+                st3s(pos + g, KP, xk);
                 double2 r[9];
                 if (!mrs_stage(&xk.x, 3, &f.x, &tq.x, 0, o.x, o.y, o.z, a.mc.scale, r)) fl |= kFlagNonFinite;
 #pragma unroll
-                for (int q = 0; q < 9; ++q) rec[q * N + g] = r[q];
+                for (int q = 0; q < 9; ++q) rec[q * KP + g] = r[q];
             }
         }
         __syncthreads();
@@ -136,7 +143,7 @@ __device__ const double* fused_front(const FusedArgs& a, double* sm, const doubl
     // phased (LJ) version
     if (vadv) {
         for (int i = tid; i < N; i += bs)
-            fl |= advance_node(src + i, vadv + i, vadv + 3 * N + i, h, a.max_disp, dst + i, N, N, N);
+            fl |= advance_node(src + i, vadv + i, vadv + 3 * KP + i, h, a.max_disp, dst + i, KP, KP, KP);
         __syncthreads();
     }
     const double* xs = vadv ? dst : src;
@@ -146,15 +153,15 @@ __device__ const double* fused_front(const FusedArgs& a, double* sm, const doubl
     double* ljf = sm + a.off_lj;
     for (int s = tid; s < nseg; s += bs) {
         const int r = s / (m - 1), k = s % (m - 1);
-        if (!rod_segment_om(a.rod, xs + m * r, k, sm[a.off_om + k], seg + 6 * s, N)) fl |= kFlagDegenerate;
+        if (!rod_segment_om(a.rod, xs + m * r, k, sm[a.off_om + k], seg + 6 * s, KP)) fl |= kFlagDegenerate;
     }
     for (int i = tid; i < N; i += bs) {
         double fx = 0, fy = 0, fz = 0;
-        const double xi = xs[i], yi = xs[N + i], zi = xs[2 * N + i];
+        const double xi = xs[i], yi = xs[KP + i], zi = xs[2 * KP + i];
         const int ri = i / m, ki = i - ri * m;
         for (int rj = 0, j = 0; rj < a.lj.rods; ++rj)
             for (int kj = 0; kj < m; ++kj, ++j)
-                lj_pair(a.lj, ri, ki, rj, kj, xi - xs[j], yi - xs[N + j], zi - xs[2 * N + j], fx, fy, fz);
+                lj_pair(a.lj, ri, ki, rj, kj, xi - xs[j], yi - xs[KP + j], zi - xs[2 * KP + j], fx, fy, fz);
         ljf[3 * i] = fx;
         ljf[3 * i + 1] = fy;
         ljf[3 * i + 2] = fz;
@@ -163,21 +170,21 @@ __device__ const double* fused_front(const FusedArgs& a, double* sm, const doubl
     for (int g = tid; g < N; g += bs) {
         const int r = g / m, k = g % m;
         d3 f, tq;
-        rod_node(a.rod, xs + m * r, seg + 6 * (m - 1) * r, k, f, tq, N);
+        rod_node(a.rod, xs + m * r, seg + 6 * (m - 1) * r, k, f, tq, KP);
         f = f + ld3(ljf + 3 * g) * a.rod.inv_ds;
-        st3s(pos + g, N, ld3s(xs + g, N));
+        st3s(pos + g, KP, ld3s(xs + g, KP));
         st3(fo + 3 * g, f);
         st3(no + 3 * g, tq);
     }
     __syncthreads();
     // stage every source relative to node 0 (the single target block's origin in mrs.cu)
-    const double ox = pos[0], oy = pos[N], oz = pos[2 * N];
+    const double ox = pos[0], oy = pos[KP], oz = pos[2 * KP];
     for (int j = tid; j < N; j += bs) {
         double2 r[9];
-        const d3 pj = ld3s(pos + j, N);
+        const d3 pj = ld3s(pos + j, KP);
         if (!mrs_stage(&pj.x, 0, fo, no, j, ox, oy, oz, a.mc.scale, r)) fl |= kFlagNonFinite;
 #pragma unroll
-        for (int q = 0; q < 9; ++q) rec[q * N + j] = r[q];
+        for (int q = 0; q < 9; ++q) rec[q * KP + j] = r[q];
     }
     __syncthreads();
     pc.mark(0);
@@ -229,13 +236,13 @@ struct MrsSplit {
     const int* cb;        // chunk bounds j0(c) = c N / C, c = 0..C (shared memory)
 };
 
-template <int CS>
-__device__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t* vbar, double t_next, PhaseClock& pc,
+template <int CS, int KP>
+__device__ __forceinline__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t* vbar, double t_next, PhaseClock& pc,
                           const MrsSplit& sp) {
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n;
     const double* pos = sm + a.off_pos;
     const double2* rec = reinterpret_cast<const double2*>(sm + a.off_rec);
-    const double ox = pos[0], oy = pos[N], oz = pos[2 * N];
+    const double ox = pos[0], oy = pos[KP], oz = pos[2 * KP];
     // MRS: this CTA owns targets [i0, i1); items (target, source chunk) computed here, the
     // chunk partials reduced locally in fixed order (mrs.cu's last-CTA reduction), and each
     // target's 6 velocities pushed to every CTA of the cluster through DSMEM.
@@ -245,13 +252,13 @@ __device__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t*
     for (int w = tid; w < nloc * a.chunks; w += bs) {
         const int c = (int)__umulhi((unsigned)w, nloc_magic), il = w - c * nloc, i = i0 + il;
         const int j0 = sp.cb[c], j1 = sp.cb[c + 1];
-        const double tx = pos[i] - ox, ty = pos[N + i] - oy, tz = pos[2 * N + i] - oz;
+        const double tx = pos[i] - ox, ty = pos[KP + i] - oy, tz = pos[2 * KP + i] - oz;
         MrsAcc acc;
         acc.zero();
 #pragma unroll 2
         for (int j = j0; j < j1; ++j)
-            mrs_pair(acc, tx, ty, tz, rec[j], rec[N + j], rec[2 * N + j], rec[3 * N + j], rec[4 * N + j],
-                     rec[5 * N + j], rec[6 * N + j], rec[7 * N + j], rec[8 * N + j], a.mc.e2, a.mc.c15e2, a.mc.cm75e4,
+            mrs_pair(acc, tx, ty, tz, rec[j], rec[KP + j], rec[2 * KP + j], rec[3 * KP + j], rec[4 * KP + j],
+                     rec[5 * KP + j], rec[6 * KP + j], rec[7 * KP + j], rec[8 * KP + j], a.mc.e2, a.mc.c15e2, a.mc.cm75e4,
                      a.mc.c25e2);
         double out[6];
         mrs_finish(acc, tx, ty, tz, out);
@@ -273,18 +280,18 @@ __device__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t*
         if constexpr (CS > 1) {
             // st.async into every CTA (itself included), completion counted on its mbarrier:
             // no cluster barrier and no GPU-scope fence per rhs
-            const uint32_t laddr = smem_u32(vel + q * N + i), lbar = smem_u32(vbar);
+            const uint32_t laddr = smem_u32(vel + q * KP + i), lbar = smem_u32(vbar);
 #pragma unroll
             for (int rr = 0; rr < CS; ++rr) st_async_f64(cluster_addr(laddr, rr), sum, cluster_addr(lbar, rr));
         } else {
-            vel[q * N + i] = sum;
+            vel[q * KP + i] = sum;
         }
     }
     if (a.prof) __syncthreads();  // phase timer only: end of the push as one CTA-wide instant
     pc.mark(4);
 }
 
-template <int CS>
+template <int CS, int KP>
 __global__ void __launch_bounds__(kFusedThreads, 1)
 fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, double dt, int scheme,
              unsigned* __restrict__ flags) {
@@ -292,8 +299,8 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n;
     double* x = sm + a.off_x;
     double* xm = sm + a.off_xm;
-    // shared-memory state: component planes [12][N] (lane-consecutive nodes, no bank conflicts)
-    for (int k = tid; k < 12 * N; k += bs) x[(k % 12) * N + k / 12] = state[k];
+    // shared-memory state: component planes [12][KP] (lane-consecutive nodes, no bank conflicts)
+    for (int k = tid; k < 12 * N; k += bs) x[(k % 12) * KP + k / 12] = state[k];
     uint64_t* vbar = reinterpret_cast<uint64_t*>(sm + a.off_bar);  // one mbarrier per velocity buffer
     if (tid == 0) {
         mbar_init(&vbar[0], 1);
@@ -330,12 +337,12 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
     double h = 0.0;
     int vp = 0;  // velocity buffer holding vadv
     for (int64_t s = 0; s < steps; ++s) {
-        double* vel = sm + a.off_vel + parity * 6 * N;
+        double* vel = sm + a.off_vel + parity * 6 * KP;
         if (vadv) vel_wait<CS>(&vbar[vp], vphase[vp], N);
         pc.mark(5);
-        fused_front<CS>(a, sm, vadv ? xb[cur ^ 1] : xb[cur], vadv, h, xb[cur], t, fl, pc);
+        fused_front<CS, KP>(a, sm, vadv ? xb[cur ^ 1] : xb[cur], vadv, h, xb[cur], t, fl, pc);
         // time of the next rhs: t + dt/2 (RK2 midpoint) or the next step's t (t += dt below)
-        fused_mrs<CS>(a, sm, vel, &vbar[parity], scheme == PSWIM_EULER ? t + dt : t + 0.5 * dt, pc, sp);
+        fused_mrs<CS, KP>(a, sm, vel, &vbar[parity], scheme == PSWIM_EULER ? t + dt : t + 0.5 * dt, pc, sp);
         const int p1 = parity;
         parity ^= 1;
         if (scheme == PSWIM_EULER) {
@@ -344,11 +351,11 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
             h = dt;
         } else {
             // step_rk2, propagators.cpp:130-133: mid = advance(x, v1, dt/2), out = advance(x, v2, dt)
-            double* vel2 = sm + a.off_vel + parity * 6 * N;
+            double* vel2 = sm + a.off_vel + parity * 6 * KP;
             vel_wait<CS>(&vbar[p1], vphase[p1], N);
             pc.mark(5);
-            fused_front<CS>(a, sm, xb[cur], vel, 0.5 * dt, xm, t + 0.5 * dt, fl, pc);
-            fused_mrs<CS>(a, sm, vel2, &vbar[parity], t + dt, pc, sp);
+            fused_front<CS, KP>(a, sm, xb[cur], vel, 0.5 * dt, xm, t + 0.5 * dt, fl, pc);
+            fused_mrs<CS, KP>(a, sm, vel2, &vbar[parity], t + dt, pc, sp);
             vp = parity;
             parity ^= 1;
             vadv = vel2;
@@ -363,12 +370,12 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
         vel_wait<CS>(&vbar[vp], vphase[vp], N);
         pc.mark(5);
         for (int i = tid; i < N; i += bs)
-            fl |= advance_node(xb[cur ^ 1] + i, vadv + i, vadv + 3 * N + i, h, a.max_disp, out + i, N, N, N);
+            fl |= advance_node(xb[cur ^ 1] + i, vadv + i, vadv + 3 * KP + i, h, a.max_disp, out + i, KP, KP, KP);
         __syncthreads();
         pc.mark(6);
     }
     if (crank == 0)
-        for (int k = tid; k < 12 * N; k += bs) state[k] = out[(k % 12) * N + k / 12];
+        for (int k = tid; k < 12 * N; k += bs) state[k] = out[(k % 12) * KP + k / 12];
     if (fl) atomicOr(flags, fl);
     cluster_barrier<CS>();  // no CTA may exit while others still push partials into it
 }
@@ -376,15 +383,15 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
 // Function attributes are set once per process, at context creation (fused_preload), never on
 // a launch path: a driver call that takes the context lock while a peer's device-side wait is
 // pending could otherwise stall another thread's launch (Parareal peer hand-offs).
-template <int CS>
+template <int CS, int KP>
 cudaError_t configure_cs() {
-    cudaError_t e = cudaFuncSetAttribute(fused_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(fused_kernel<CS, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess && CS > 8)
-        e = cudaFuncSetAttribute(fused_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        e = cudaFuncSetAttribute(fused_kernel<CS, KP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return e;
 }
 
-template <int CS>
+template <int CS, int KP>
 cudaError_t launch_cs(const FusedArgs& a, size_t smem, double* state, int64_t steps, double t0, double dt, int scheme,
                       unsigned* flags, cudaStream_t st) {
     // (function attributes: configure_cs, run by fused_preload at context creation)
@@ -400,7 +407,42 @@ cudaError_t launch_cs(const FusedArgs& a, size_t smem, double* state, int64_t st
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, fused_kernel<CS>, a, state, steps, t0, dt, scheme, flags);
+    return cudaLaunchKernelEx(&cfg, fused_kernel<CS, KP>, a, state, steps, t0, dt, scheme, flags);
+}
+
+// Shared-memory layout of a fused launch (offsets in doubles, 16-B aligned) into a; returns the
+// doubles used.  Planes of stride KP: x, xm, x2 (12 each), pos (3), rec (18 = 9 double2),
+// velocities (2 x 6); the warp-tiled front's tiles (fast path) share one region with the
+// phased path's f / n / lj / segment buffers (LJ systems), which never coexist.
+int64_t fused_layout(const RodParams& p, const MrsPlan& plan, int cs, FusedArgs& a) {
+    const int64_t n = p.rods * p.m, kp = n <= 128 ? 128 : 256, tpc = (n + cs - 1) / cs;
+    int64_t off = 0;
+    auto take = [&](int64_t count) {
+        const int64_t o = off;
+        off += (count + 1) & ~int64_t(1);  // keep 16-B alignment
+        return (int)o;
+    };
+    a.off_x = take(12 * kp);
+    a.off_xm = take(12 * kp);
+    a.off_x2 = take(12 * kp);
+    a.off_pos = take(3 * kp);
+    a.off_rec = take(18 * kp);
+    a.off_vel = take(12 * kp);
+    a.off_part = take(plan.chunks * tpc * 6);
+    a.part_stride = 0;
+    const int64_t shared = off;  // union: front tiles | f, n, lj, seg
+    a.off_tile = take(((n + kFrontNodes - 1) / kFrontNodes) * 32 * 12);
+    const int64_t after_tiles = off;
+    off = shared;
+    a.off_f = take(3 * n);
+    a.off_n = take(3 * n);
+    a.off_lj = take(3 * n);
+    a.off_seg = take(6 * p.rods * (p.m - 1));
+    off = std::max(off, after_tiles);
+    a.off_bar = take(2);
+    a.off_om = take(p.m);
+    a.off_cb = take((plan.chunks + 2) / 2);
+    return off;
 }
 
 }  // namespace
@@ -425,32 +467,38 @@ int fused_cluster_size(const RodParams& p, int max_hint) {
     const int min_tpc = max_hint >= 16 ? 6 : min_tpc_env;
     int cs = 1;
     while (cs < max_cs && (n + 2 * cs - 1) / (2 * cs) >= min_tpc) cs *= 2;  // >= min_tpc targets per CTA
-    const int64_t tpc = (n + cs - 1) / cs;
-    // shared memory: x, xm (12n each), pos/f/n/lj (3n each), seg, rec (18n), local partials
-    // (chunks x tpc x 6), velocities (2 x 6n), x2 (12n), front tiles (warps x 32 x 12)
-    const int64_t doubles = 24 * n + 12 * n + 6 * p.rods * (p.m - 1) + 18 * n + plan.chunks * tpc * 6 + 12 * n + 16 +
-                            12 * n + ((n + kFrontNodes - 1) / kFrontNodes) * 32 * 12 + 2 + p.m + 1 +
-                            (plan.chunks + 2) / 2 + 1;
+    FusedArgs a;
+    const int64_t doubles = fused_layout(p, plan, cs, a);
     if (doubles * 8 > 220 * 1024) return 0;
     return cs;
 }
 
 void fused_preload() {
     static const bool once = [] {
-        configure_cs<1>();
-        configure_cs<2>();
-        configure_cs<4>();
-        configure_cs<8>();
-        configure_cs<16>();
+        configure_cs<1, 128>();
+        configure_cs<2, 128>();
+        configure_cs<4, 128>();
+        configure_cs<8, 128>();
+        configure_cs<16, 128>();
+        configure_cs<1, 256>();
+        configure_cs<2, 256>();
+        configure_cs<4, 256>();
+        configure_cs<8, 256>();
+        configure_cs<16, 256>();
         return true;
     }();
     (void)once;
     cudaFuncAttributes a;
-    cudaFuncGetAttributes(&a, fused_kernel<1>);
-    cudaFuncGetAttributes(&a, fused_kernel<2>);
-    cudaFuncGetAttributes(&a, fused_kernel<4>);
-    cudaFuncGetAttributes(&a, fused_kernel<8>);
-    cudaFuncGetAttributes(&a, fused_kernel<16>);
+    cudaFuncGetAttributes(&a, fused_kernel<1, 128>);
+    cudaFuncGetAttributes(&a, fused_kernel<2, 128>);
+    cudaFuncGetAttributes(&a, fused_kernel<4, 128>);
+    cudaFuncGetAttributes(&a, fused_kernel<8, 128>);
+    cudaFuncGetAttributes(&a, fused_kernel<16, 128>);
+    cudaFuncGetAttributes(&a, fused_kernel<1, 256>);
+    cudaFuncGetAttributes(&a, fused_kernel<2, 256>);
+    cudaFuncGetAttributes(&a, fused_kernel<4, 256>);
+    cudaFuncGetAttributes(&a, fused_kernel<8, 256>);
+    cudaFuncGetAttributes(&a, fused_kernel<16, 256>);
 }
 
 cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t steps, double t0, double dt, int scheme,
@@ -471,36 +519,23 @@ cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t st
     a.lj_on = (p.rods >= 2 && p.lj_well > 0.0) ? 1 : 0;  // propagators.cpp:70
     a.max_disp = 10.0 * p.ds;
     a.prof = prof;
-    int off = 0;
-    auto take = [&](int count) {
-        const int o = off;
-        off += (count + 1) & ~1;  // keep 16-B alignment
-        return o;
-    };
-    a.off_x = take(12 * a.n);
-    a.off_xm = take(12 * a.n);
-    a.off_pos = take(3 * a.n);
-    a.off_f = take(3 * a.n);
-    a.off_n = take(3 * a.n);
-    a.off_seg = take(6 * a.rods * (a.m - 1));
-    a.off_lj = take(3 * a.n);
-    a.off_rec = take(18 * a.n);
-    const int tpc = (a.n + cs - 1) / cs;
-    a.part_stride = 0;
-    a.off_part = take(plan.chunks * tpc * 6);
-    a.off_vel = take(12 * a.n);
-    a.off_x2 = take(12 * a.n);
-    a.off_tile = take(((a.n + kFrontNodes - 1) / kFrontNodes) * 32 * 12);
-    a.off_bar = take(2);
-    a.off_om = take(a.m);
-    a.off_cb = take((plan.chunks + 2) / 2);
-    const size_t smem = (size_t)off * sizeof(double);
+    const int64_t doubles = fused_layout(p, plan, cs, a);
+    const size_t smem = (size_t)doubles * sizeof(double);
+    if (n <= 128) {
+        switch (cs) {
+            case 1: return launch_cs<1, 128>(a, smem, state, steps, t0, dt, scheme, flags, st);
+            case 2: return launch_cs<2, 128>(a, smem, state, steps, t0, dt, scheme, flags, st);
+            case 4: return launch_cs<4, 128>(a, smem, state, steps, t0, dt, scheme, flags, st);
+            case 8: return launch_cs<8, 128>(a, smem, state, steps, t0, dt, scheme, flags, st);
+            default: return launch_cs<16, 128>(a, smem, state, steps, t0, dt, scheme, flags, st);
+        }
+    }
     switch (cs) {
-        case 1: return launch_cs<1>(a, smem, state, steps, t0, dt, scheme, flags, st);
-        case 2: return launch_cs<2>(a, smem, state, steps, t0, dt, scheme, flags, st);
-        case 4: return launch_cs<4>(a, smem, state, steps, t0, dt, scheme, flags, st);
-        case 8: return launch_cs<8>(a, smem, state, steps, t0, dt, scheme, flags, st);
-        default: return launch_cs<16>(a, smem, state, steps, t0, dt, scheme, flags, st);
+        case 1: return launch_cs<1, 256>(a, smem, state, steps, t0, dt, scheme, flags, st);
+        case 2: return launch_cs<2, 256>(a, smem, state, steps, t0, dt, scheme, flags, st);
+        case 4: return launch_cs<4, 256>(a, smem, state, steps, t0, dt, scheme, flags, st);
+        case 8: return launch_cs<8, 256>(a, smem, state, steps, t0, dt, scheme, flags, st);
+        default: return launch_cs<16, 256>(a, smem, state, steps, t0, dt, scheme, flags, st);
     }
 }
 
