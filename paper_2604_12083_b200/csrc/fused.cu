@@ -56,14 +56,17 @@ struct FusedArgs {
 // by thread 0 of cluster rank 0 (the stage timers of propagators.hpp:55-65 for a path that is
 // one kernel).  Phases: 0 segment loads (+LJ), 1 nodal loads, 2 MRS source staging, 3 MRS
 // pairs, 4 chunk reduction + DSMEM velocity push, 5 cluster barrier, 6 advance.
+template <bool kOn>
 struct PhaseClock {
     unsigned long long* prof;
     long long t;
     __device__ __forceinline__ void mark(int phase) {
-        if (prof) {
-            const long long c = clock64();
-            prof[phase] += (unsigned long long)(c - t);
-            t = c;
+        if constexpr (kOn) {
+            if (prof) {
+                const long long c = clock64();
+                prof[phase] += (unsigned long long)(c - t);
+                t = c;
+            }
         }
     }
 };
@@ -80,16 +83,16 @@ __device__ __forceinline__ void cluster_barrier() {
 // Front half of an rhs (propagators.cpp:38-91): produce the rhs state -- `src` itself
 // (vadv == nullptr) or dst = advance_state(src, vadv, h) node by node (propagators.cpp:93-124)
 // -- and, on that state, the segment and nodal loads and the MRS source records (rec) and
-// target positions (pos).  Returns the rhs state.
+// target positions (pos).
 //
 // Systems without LJ take a warp-tiled pass with no CTA barrier inside: warp w covers nodes
 // 30 w - 1 + lane (lanes 1..30 own a node, lanes 0 and 31 recompute a neighbour's advance),
 // advances them into a per-warp tile, computes segment (g, g+1) per lane and gets segment
 // g - 1 by one shuffle -- the layout of rod_loads_wtma_kernel.  LJ needs every advanced
 // position first, so LJ systems take the phased version.
-template <int CS, int KP>
-__device__ __forceinline__ const double* fused_front(const FusedArgs& a, double* sm, const double* src, const double* vadv, double h,
-                                     double* dst, double t, unsigned& fl, PhaseClock& pc) {
+template <int CS, int KP, bool kProf>
+__device__ __forceinline__ void fused_front(const FusedArgs& a, double* sm, const double* src, const double* vadv, double h,
+                                            double* dst, unsigned& fl, PhaseClock<kProf>& pc) {
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n, m = a.m, nseg = a.rods * (m - 1);
     double* pos = sm + a.off_pos;
     double2* rec = reinterpret_cast<double2*>(sm + a.off_rec);
@@ -138,7 +141,7 @@ __device__ __forceinline__ const double* fused_front(const FusedArgs& a, double*
         }
         __syncthreads();
         pc.mark(0);
-        return vadv ? dst : src;
+        return;
     }
     // phased (LJ) version
     if (vadv) {
@@ -188,7 +191,6 @@ __device__ __forceinline__ const double* fused_front(const FusedArgs& a, double*
     }
     __syncthreads();
     pc.mark(0);
-    return xs;
 }
 
 // Back half of an rhs: the O(N^2) MRS of the staged sources into vel[6 n] = (u, w) per node.
@@ -209,12 +211,13 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t 
 // Wait until this CTA's velocity buffer of the given mbarrier holds all N x 6 values of the
 // rhs (every CTA's st.async pushes counted as transaction bytes): thread 0 posts the
 // expected bytes and the one arrival, every thread waits on the phase parity.
+// `phases` holds one phase-parity bit per velocity buffer (a register, not a local array).
 template <int CS>
-__device__ __forceinline__ void vel_wait(uint64_t* vbar, uint32_t& phase, int n) {
+__device__ __forceinline__ void vel_wait(uint64_t* vbar, uint32_t& phases, int buf, int n) {
     if constexpr (CS > 1) {
         if (threadIdx.x == 0) mbar_expect_tx(vbar, (uint32_t)(6 * n * sizeof(double)));
-        mbar_wait(vbar, phase & 1u);
-        ++phase;
+        mbar_wait(vbar, (phases >> buf) & 1u);
+        phases ^= 1u << buf;
     } else {
         __syncthreads();
     }
@@ -236,9 +239,9 @@ struct MrsSplit {
     const int* cb;        // chunk bounds j0(c) = c N / C, c = 0..C (shared memory)
 };
 
-template <int CS, int KP>
-__device__ __forceinline__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t* vbar, double t_next, PhaseClock& pc,
-                          const MrsSplit& sp) {
+template <int CS, int KP, bool kProf>
+__device__ __forceinline__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t* vbar, double t_next,
+                                          PhaseClock<kProf>& pc, const MrsSplit& sp) {
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n;
     const double* pos = sm + a.off_pos;
     const double2* rec = reinterpret_cast<const double2*>(sm + a.off_rec);
@@ -287,27 +290,24 @@ __device__ __forceinline__ void fused_mrs(const FusedArgs& a, double* sm, double
             vel[q * KP + i] = sum;
         }
     }
-    if (a.prof) __syncthreads();  // phase timer only: end of the push as one CTA-wide instant
+    if constexpr (kProf) __syncthreads();  // phase timer only: end of the push as one CTA-wide instant
     pc.mark(4);
 }
 
-template <int CS, int KP>
+template <int CS, int KP, bool kProf>
 __global__ void __launch_bounds__(kFusedThreads, 1)
 fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, double dt, int scheme,
              unsigned* __restrict__ flags) {
     extern __shared__ __align__(16) double sm[];
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n;
-    double* x = sm + a.off_x;
-    double* xm = sm + a.off_xm;
     // shared-memory state: component planes [12][KP] (lane-consecutive nodes, no bank conflicts)
-    for (int k = tid; k < 12 * N; k += bs) x[(k % 12) * KP + k / 12] = state[k];
+    for (int k = tid; k < 12 * N; k += bs) sm[a.off_x + (k % 12) * KP + k / 12] = state[k];
     uint64_t* vbar = reinterpret_cast<uint64_t*>(sm + a.off_bar);  // one mbarrier per velocity buffer
     if (tid == 0) {
         mbar_init(&vbar[0], 1);
         mbar_init(&vbar[1], 1);
         fence_mbar_init();
     }
-    uint32_t vphase[2] = {0u, 0u};
     strain_table(a, sm, t0);
     MrsSplit sp;
     {
@@ -322,55 +322,46 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
     }
     cluster_barrier<CS>();  // barriers initialised before any CTA pushes into them
     unsigned fl = 0;
-    int parity = 0;
-    double t = t0;
     const int crank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
-    PhaseClock pc{(a.prof && tid == 0 && crank == 0) ? a.prof : nullptr, clock64()};
-    // velocities are double-buffered: a CTA that runs ahead pushes the next rhs into the
-    // other buffer while slower CTAs still read this one (the next cluster barrier orders it).
-    // The advance that produces an rhs state runs inside that rhs's front pass (src -> dst,
-    // never in place: overlap lanes read neighbours' old states), so the step-start state
-    // alternates between x and x2; xm holds the RK2 midpoint.
-    double* xb[2] = {x, sm + a.off_x2};
-    int cur = 0;
-    const double* vadv = nullptr;  // velocities of the pending advance (none before step 0)
-    double h = 0.0;
-    int vp = 0;  // velocity buffer holding vadv
-    for (int64_t s = 0; s < steps; ++s) {
-        double* vel = sm + a.off_vel + parity * 6 * KP;
-        if (vadv) vel_wait<CS>(&vbar[vp], vphase[vp], N);
+    PhaseClock<kProf> pc{(kProf && tid == 0 && crank == 0) ? a.prof : nullptr, clock64()};
+    // One loop iteration per rhs (one call site of each phase: half the code of a per-step
+    // body, which matters for the instruction cache).  Buffers are picked by shared-memory
+    // offsets (no runtime-indexed local arrays, so every state access stays an LDS):
+    //   * step s starts from state buffer S(s) = x (s even) / x2 (s odd); the advance that
+    //     produces an rhs state runs inside that rhs's front pass, never in place (overlap
+    //     lanes read neighbours' old states); xm holds the RK2 midpoint;
+    //   * rhs r writes velocity buffer r & 1 (double-buffered: a CTA that runs ahead pushes
+    //     the next rhs into the other buffer while slower CTAs still read this one).
+    // step_rk2 (propagators.cpp:130-133): mid = advance(S(s), v1, dt/2), S(s+1) = advance(S(s), v2, dt).
+    const bool rk2 = scheme != PSWIM_EULER;
+    const int64_t nrhs = rk2 ? 2 * steps : steps;
+    uint32_t vph = 0u;  // phase-parity bit per velocity buffer
+    double t = t0;
+    for (int64_t r = 0; r < nrhs; ++r) {
+        const int p = (int)(r & 1);
+        const bool mid = rk2 && p;  // the RK2 midpoint rhs
+        const int64_t s = rk2 ? (r >> 1) : r;
+        const int o_start = (s & 1) ? a.off_x2 : a.off_x, o_prev = (s & 1) ? a.off_x : a.off_x2;
+        const double* vadv = r > 0 ? sm + a.off_vel + (p ^ 1) * 6 * KP : nullptr;
+        if (r > 0) vel_wait<CS>(&vbar[p ^ 1], vph, p ^ 1, N);
         pc.mark(5);
-        fused_front<CS, KP>(a, sm, vadv ? xb[cur ^ 1] : xb[cur], vadv, h, xb[cur], t, fl, pc);
+        const double* src = sm + (mid ? o_start : (r > 0 ? o_prev : o_start));
+        double* dst = sm + (mid ? a.off_xm : o_start);
+        fused_front<CS, KP, kProf>(a, sm, src, vadv, mid ? 0.5 * dt : dt, dst, fl, pc);
         // time of the next rhs: t + dt/2 (RK2 midpoint) or the next step's t (t += dt below)
-        fused_mrs<CS, KP>(a, sm, vel, &vbar[parity], scheme == PSWIM_EULER ? t + dt : t + 0.5 * dt, pc, sp);
-        const int p1 = parity;
-        parity ^= 1;
-        if (scheme == PSWIM_EULER) {
-            vadv = vel;
-            vp = p1;
-            h = dt;
-        } else {
-            // step_rk2, propagators.cpp:130-133: mid = advance(x, v1, dt/2), out = advance(x, v2, dt)
-            double* vel2 = sm + a.off_vel + parity * 6 * KP;
-            vel_wait<CS>(&vbar[p1], vphase[p1], N);
-            pc.mark(5);
-            fused_front<CS, KP>(a, sm, xb[cur], vel, 0.5 * dt, xm, t + 0.5 * dt, fl, pc);
-            fused_mrs<CS, KP>(a, sm, vel2, &vbar[parity], t + dt, pc, sp);
-            vp = parity;
-            parity ^= 1;
-            vadv = vel2;
-            h = dt;
-        }
-        cur ^= 1;  // the next state goes to the other buffer
-        t += dt;   // propagators.cpp:159
+        fused_mrs<CS, KP, kProf>(a, sm, sm + a.off_vel + p * 6 * KP, &vbar[p], rk2 && !mid ? t + 0.5 * dt : t + dt, pc, sp);
+        if (!rk2 || mid) t += dt;  // propagators.cpp:159
     }
-    // the last step's closing advance (no rhs follows)
-    double* out = xb[cur];
-    if (vadv) {
-        vel_wait<CS>(&vbar[vp], vphase[vp], N);
+    // the last step's closing advance (no rhs follows): S(steps) = advance(S(steps - 1), v, dt)
+    double* out = sm + ((steps & 1) ? a.off_x2 : a.off_x);
+    if (nrhs > 0) {
+        const int pl = (int)((nrhs - 1) & 1);
+        const double* vadv = sm + a.off_vel + pl * 6 * KP;
+        const double* src = sm + ((steps & 1) ? a.off_x : a.off_x2);
+        vel_wait<CS>(&vbar[pl], vph, pl, N);
         pc.mark(5);
         for (int i = tid; i < N; i += bs)
-            fl |= advance_node(xb[cur ^ 1] + i, vadv + i, vadv + 3 * KP + i, h, a.max_disp, out + i, KP, KP, KP);
+            fl |= advance_node(src + i, vadv + i, vadv + 3 * KP + i, dt, a.max_disp, out + i, KP, KP, KP);
         __syncthreads();
         pc.mark(6);
     }
@@ -383,16 +374,29 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
 // Function attributes are set once per process, at context creation (fused_preload), never on
 // a launch path: a driver call that takes the context lock while a peer's device-side wait is
 // pending could otherwise stall another thread's launch (Parareal peer hand-offs).
-template <int CS, int KP>
-cudaError_t configure_cs() {
-    cudaError_t e = cudaFuncSetAttribute(fused_kernel<CS, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+template <int CS, int KP, bool kProf>
+cudaError_t configure_one() {
+    cudaError_t e = cudaFuncSetAttribute(fused_kernel<CS, KP, kProf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess && CS > 8)
-        e = cudaFuncSetAttribute(fused_kernel<CS, KP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        e = cudaFuncSetAttribute(fused_kernel<CS, KP, kProf>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return e;
 }
 
 template <int CS, int KP>
-cudaError_t launch_cs(const FusedArgs& a, size_t smem, double* state, int64_t steps, double t0, double dt, int scheme,
+void load_cs() {
+    cudaFuncAttributes fa;  // loads the module on the current device (lazy loading)
+    cudaFuncGetAttributes(&fa, fused_kernel<CS, KP, false>);
+    cudaFuncGetAttributes(&fa, fused_kernel<CS, KP, true>);
+}
+
+template <int CS, int KP>
+void configure_cs() {
+    configure_one<CS, KP, false>();
+    configure_one<CS, KP, true>();
+}
+
+template <int CS, int KP, bool kProf>
+cudaError_t launch_one(const FusedArgs& a, size_t smem, double* state, int64_t steps, double t0, double dt, int scheme,
                       unsigned* flags, cudaStream_t st) {
     // (function attributes: configure_cs, run by fused_preload at context creation)
     cudaLaunchConfig_t cfg{};
@@ -407,7 +411,16 @@ cudaError_t launch_cs(const FusedArgs& a, size_t smem, double* state, int64_t st
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, fused_kernel<CS, KP>, a, state, steps, t0, dt, scheme, flags);
+    return cudaLaunchKernelEx(&cfg, fused_kernel<CS, KP, kProf>, a, state, steps, t0, dt, scheme, flags);
+}
+
+// the phase-timer instantiation only for pswim_fused_profile: the production kernel has no
+// timer code at all
+template <int CS, int KP>
+cudaError_t launch_cs(const FusedArgs& a, size_t smem, double* state, int64_t steps, double t0, double dt, int scheme,
+                      unsigned* flags, cudaStream_t st) {
+    return a.prof ? launch_one<CS, KP, true>(a, smem, state, steps, t0, dt, scheme, flags, st)
+                  : launch_one<CS, KP, false>(a, smem, state, steps, t0, dt, scheme, flags, st);
 }
 
 // Shared-memory layout of a fused launch (offsets in doubles, 16-B aligned) into a; returns the
@@ -474,6 +487,8 @@ int fused_cluster_size(const RodParams& p, int max_hint) {
 }
 
 void fused_preload() {
+    // attributes set once per process, modules loaded on every device that creates a context
+    // (every launch path stays free of attribute calls and lazy-loading synchronisation)
     static const bool once = [] {
         configure_cs<1, 128>();
         configure_cs<2, 128>();
@@ -488,17 +503,16 @@ void fused_preload() {
         return true;
     }();
     (void)once;
-    cudaFuncAttributes a;
-    cudaFuncGetAttributes(&a, fused_kernel<1, 128>);
-    cudaFuncGetAttributes(&a, fused_kernel<2, 128>);
-    cudaFuncGetAttributes(&a, fused_kernel<4, 128>);
-    cudaFuncGetAttributes(&a, fused_kernel<8, 128>);
-    cudaFuncGetAttributes(&a, fused_kernel<16, 128>);
-    cudaFuncGetAttributes(&a, fused_kernel<1, 256>);
-    cudaFuncGetAttributes(&a, fused_kernel<2, 256>);
-    cudaFuncGetAttributes(&a, fused_kernel<4, 256>);
-    cudaFuncGetAttributes(&a, fused_kernel<8, 256>);
-    cudaFuncGetAttributes(&a, fused_kernel<16, 256>);
+    load_cs<1, 128>();
+    load_cs<2, 128>();
+    load_cs<4, 128>();
+    load_cs<8, 128>();
+    load_cs<16, 128>();
+    load_cs<1, 256>();
+    load_cs<2, 256>();
+    load_cs<4, 256>();
+    load_cs<8, 256>();
+    load_cs<16, 256>();
 }
 
 cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t steps, double t0, double dt, int scheme,
