@@ -919,7 +919,7 @@ def latency_roofline(ctx, sc, cs, steps_per_s, clocks):
     import math
 
     n = sc.total_nodes
-    chunks = max(1, (n + 3) // 4)  # mrs_plan's single-block small-system plan
+    chunks = max(1, (n + 5) // 6)  # mrs_plan's single-block small-system plan (6 sources per chunk)
     tpc = (n + cs - 1) // cs
     warps = math.ceil(tpc * chunks / 32)
     ns = math.ceil(n / chunks)

@@ -1,5 +1,6 @@
 """Dev sweep: fused-kernel per-rhs phase floors (pswim_dev_latency_probe) for alternative MRS
-item decompositions of the 100-node flagellum on a 16-CTA cluster (7 targets per CTA)."""
+item decompositions of an N-node system with tpc targets per CTA (N = 100: tpc 7 on a
+16-CTA cluster, 13 on 8 CTAs)."""
 import ctypes as C
 import math
 import os
@@ -11,14 +12,14 @@ from paper_2604_12083_b200.scenario import ScenarioConfig, make_scenario
 
 sc = make_scenario(ScenarioConfig(rod_count=1, nodes_per_rod=100))
 ctx = Context(0, sc)
-n, tpc = 100, 7
-for ns in (1, 2, 3, 4, 5, 6, 8):
-    chunks = math.ceil(n / ns)
-    warps = math.ceil(tpc * chunks / 32)
-    for w in sorted({min(warps, 12), 12, 8, 6, 4}):
-        if w < min(warps, 12):
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 100
+for tpc in [int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else "7,13").split(",")]:
+    for ns in (2, 3, 4, 5, 6, 7, 8):
+        chunks = math.ceil(n / ns)
+        warps = math.ceil(tpc * chunks / 32)
+        if warps > 12:
             continue
         out = (C.c_double * 4)()
-        rc = ctx.lib.pswim_dev_latency_probe(ctx.handle, ns, w, min(chunks, 64), 6 * tpc, 6 * n, out)
-        print(f"ns {ns} chunks {chunks} item-warps needed {warps} run on {w}: front {out[0]:.0f} items {out[1]:.0f} "
-              f"reduce {out[2]:.0f} exchange {out[3]:.0f} rc {rc}")
+        rc = ctx.lib.pswim_dev_latency_probe(ctx.handle, ns, warps, min(chunks, 64), 6 * tpc, 6 * n, out)
+        print(f"n {n} tpc {tpc} ns {ns} chunks {chunks} warps {warps}: items {out[1]:.0f} reduce {out[2]:.0f} "
+              f"sum {out[1] + out[2]:.0f} rc {rc}")
