@@ -39,6 +39,7 @@ struct FusedArgs {
     int n;        // total nodes
     int rods, m;  // layout
     int chunks;   // MRS source chunks (== mrs_plan(n, n).chunks)
+    int chunk_fixed;  // mrs_plan(n, n).fixed: sources per chunk (0: c N / C bounds)
     unsigned m_magic;  // __umulhi(g, m_magic) == g / m for g, m < 2^16 (no division on the chains)
     int lj_on;
     double max_disp;
@@ -46,7 +47,7 @@ struct FusedArgs {
     int off_x, off_xm, off_pos, off_f, off_n, off_seg, off_lj, off_rec, off_part, off_vel;
     int off_x2, off_tile;  // second step-start state buffer; per-warp front tiles (32 x 12)
     int off_bar;           // two mbarriers (velocity buffers)
-    int off_om;            // preferred strain per segment index at the coming rhs time (m - 1)
+    int off_om;            // preferred strain per segment index (m - 1), two tables: rhs r reads r & 1
     int off_cb;            // MRS chunk bounds (chunks + 1 ints)
     int part_stride;  // unused (kept for layout clarity)
     unsigned long long* prof;  // kFusedPhases clock64 counters (CTA 0, thread 0), nullptr = off
@@ -80,6 +81,14 @@ __device__ __forceinline__ void cluster_barrier() {
     }
 }
 
+// The preferred strain of every segment index at time t (rod.cpp:29-32) into table `om`:
+// `sin` leaves the segment chains of the front pass (the same explicit-rounding rod_strain as
+// every kernel).  Filled from the top thread down.
+__device__ __forceinline__ void strain_table(const FusedArgs& a, double* om, double t) {
+    for (int k = (int)blockDim.x - 1 - (int)threadIdx.x; k >= 0; k -= (int)blockDim.x)
+        if (k < a.m - 1) om[k] = rod_strain(a.rod, k, t);
+}
+
 // Front half of an rhs (propagators.cpp:38-91): produce the rhs state -- `src` itself
 // (vadv == nullptr) or dst = advance_state(src, vadv, h) node by node (propagators.cpp:93-124)
 // -- and, on that state, the segment and nodal loads and the MRS source records (rec) and
@@ -92,13 +101,18 @@ __device__ __forceinline__ void cluster_barrier() {
 // position first, so LJ systems take the phased version.
 template <int CS, int KP, bool kProf>
 __device__ __forceinline__ void fused_front(const FusedArgs& a, double* sm, const double* src, const double* vadv, double h,
-                                            double* dst, unsigned& fl, PhaseClock<kProf>& pc) {
+                                            double* dst, const double* om, double* om_next, double t_next, unsigned& fl,
+                                            PhaseClock<kProf>& pc) {
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n, m = a.m, nseg = a.rods * (m - 1);
     double* pos = sm + a.off_pos;
     double2* rec = reinterpret_cast<double2*>(sm + a.off_rec);
     if (!a.lj_on) {
         const int warp = tid >> 5, lane = tid & 31, nw = (N + kFrontNodes - 1) / kFrontNodes;
-        if (warp < nw) {
+        if (warp >= nw) {
+            // the warps without front nodes tabulate the next rhs's preferred strain meanwhile
+            // (its sin chains leave the MRS phase)
+            for (int k = tid - 32 * nw; k < a.m - 1; k += bs - 32 * nw) om_next[k] = rod_strain(a.rod, k, t_next);
+        } else {
             const int base = kFrontNodes * warp - 1, g = base + lane;
             const bool valid = g >= 0 && g < N;
             double* tile = sm + a.off_tile + warp * 32 * 12;  // planes [12][32]: slot l = node base + l
@@ -121,7 +135,7 @@ __device__ __forceinline__ void fused_front(const FusedArgs& a, double* sm, cons
             constexpr int xc = 32;
             double seg[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             if (valid && lane < 31 && k + 1 < m)
-                if (!rod_segment_om(a.rod, xs, k, sm[a.off_om + k], seg, xc)) fl |= kFlagDegenerate;
+                if (!rod_segment_om(a.rod, xs, k, om[k], seg, xc)) fl |= kFlagDegenerate;
             double prev[6];
 #pragma unroll
             for (int q = 0; q < 6; ++q) prev[q] = __shfl_up_sync(0xffffffffu, seg[q], 1);
@@ -156,7 +170,7 @@ __device__ __forceinline__ void fused_front(const FusedArgs& a, double* sm, cons
     double* ljf = sm + a.off_lj;
     for (int s = tid; s < nseg; s += bs) {
         const int r = s / (m - 1), k = s % (m - 1);
-        if (!rod_segment_om(a.rod, xs + m * r, k, sm[a.off_om + k], seg + 6 * s, KP)) fl |= kFlagDegenerate;
+        if (!rod_segment_om(a.rod, xs + m * r, k, om[k], seg + 6 * s, KP)) fl |= kFlagDegenerate;
     }
     for (int i = tid; i < N; i += bs) {
         double fx = 0, fy = 0, fz = 0;
@@ -180,6 +194,7 @@ __device__ __forceinline__ void fused_front(const FusedArgs& a, double* sm, cons
         st3(no + 3 * g, tq);
     }
     __syncthreads();
+    strain_table(a, om_next, t_next);  // (this rhs's segment pass is done: barrier above)
     // stage every source relative to node 0 (the single target block's origin in mrs.cu)
     const double ox = pos[0], oy = pos[KP], oz = pos[2 * KP];
     for (int j = tid; j < N; j += bs) {
@@ -223,14 +238,6 @@ __device__ __forceinline__ void vel_wait(uint64_t* vbar, uint32_t& phases, int b
     }
 }
 
-// The preferred strain of every segment index at time t (rod.cpp:29-32) into the CTA's table:
-// `sin` leaves the segment chains of the front pass.  Filled from the top thread down, so the
-// threads without MRS items take it (the same explicit-rounding rod_strain as every kernel).
-__device__ __forceinline__ void strain_table(const FusedArgs& a, double* sm, double t) {
-    for (int k = (int)blockDim.x - 1 - (int)threadIdx.x; k >= 0; k -= (int)blockDim.x)
-        if (k < a.m - 1) sm[a.off_om + k] = rod_strain(a.rod, k, t);
-}
-
 // This CTA's MRS targets [i0, i0 + nloc) of the cluster split (tpc per CTA), fixed for the
 // launch: computed once, not per rhs (the divisions sat on every rhs's MRS path).
 struct MrsSplit {
@@ -240,7 +247,7 @@ struct MrsSplit {
 };
 
 template <int CS, int KP, bool kProf>
-__device__ __forceinline__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t* vbar, double t_next,
+__device__ __forceinline__ void fused_mrs(const FusedArgs& a, double* sm, double* vel, uint64_t* vbar,
                                           PhaseClock<kProf>& pc, const MrsSplit& sp) {
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n;
     const double* pos = sm + a.off_pos;
@@ -268,8 +275,6 @@ __device__ __forceinline__ void fused_mrs(const FusedArgs& a, double* sm, double
 #pragma unroll
         for (int q = 0; q < 6; ++q) lpart[(c * 6 + q) * tpc + il] = out[q];  // [chunk][component][target]
     }
-    // the next rhs's strain table (this rhs's front pass has read it: barrier at its end)
-    strain_table(a, sm, t_next);
     __syncthreads();
     pc.mark(3);
     // one thread per (target, component): the chunk partials summed in chunk order 0..C-1
@@ -308,7 +313,7 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
         mbar_init(&vbar[1], 1);
         fence_mbar_init();
     }
-    strain_table(a, sm, t0);
+    strain_table(a, sm + a.off_om, t0);  // table 0: rhs 0
     MrsSplit sp;
     {
         const int rank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
@@ -317,7 +322,9 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
         sp.nloc = max(0, min(N, sp.i0 + sp.tpc) - sp.i0);
         sp.nloc_magic = sp.nloc > 0 ? 0xFFFFFFFFu / (unsigned)sp.nloc + 1u : 0u;
         int* cb = reinterpret_cast<int*>(sm + a.off_cb);
-        for (int c = tid; c <= a.chunks; c += bs) cb[c] = c * N / a.chunks;  // (N <= 256: no overflow)
+        // the plan's chunk bounds (mrs_chunk_bound): c N / C, or `fixed` sources per chunk
+        for (int c = tid; c <= a.chunks; c += bs)
+            cb[c] = a.chunk_fixed > 0 ? min(c * a.chunk_fixed, N) : c * N / a.chunks;  // (N <= 256: no overflow)
         sp.cb = cb;
     }
     cluster_barrier<CS>();  // barriers initialised before any CTA pushes into them
@@ -347,9 +354,11 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
         pc.mark(5);
         const double* src = sm + (mid ? o_start : (r > 0 ? o_prev : o_start));
         double* dst = sm + (mid ? a.off_xm : o_start);
-        fused_front<CS, KP, kProf>(a, sm, src, vadv, mid ? 0.5 * dt : dt, dst, fl, pc);
-        // time of the next rhs: t + dt/2 (RK2 midpoint) or the next step's t (t += dt below)
-        fused_mrs<CS, KP, kProf>(a, sm, sm + a.off_vel + p * 6 * KP, &vbar[p], rk2 && !mid ? t + 0.5 * dt : t + dt, pc, sp);
+        // strain tables: this rhs reads table p; the next rhs's (at t + dt/2 for the RK2
+        // midpoint, else the next step's t; t += dt below) goes to table p ^ 1 meanwhile
+        fused_front<CS, KP, kProf>(a, sm, src, vadv, mid ? 0.5 * dt : dt, dst, sm + a.off_om + p * a.m,
+                                   sm + a.off_om + (p ^ 1) * a.m, rk2 && !mid ? t + 0.5 * dt : t + dt, fl, pc);
+        fused_mrs<CS, KP, kProf>(a, sm, sm + a.off_vel + p * 6 * KP, &vbar[p], pc, sp);
         if (!rk2 || mid) t += dt;  // propagators.cpp:159
     }
     // the last step's closing advance (no rhs follows): S(steps) = advance(S(steps - 1), v, dt)
@@ -453,7 +462,7 @@ int64_t fused_layout(const RodParams& p, const MrsPlan& plan, int cs, FusedArgs&
     a.off_seg = take(6 * p.rods * (p.m - 1));
     off = std::max(off, after_tiles);
     a.off_bar = take(2);
-    a.off_om = take(p.m);
+    a.off_om = take(2 * p.m);
     a.off_cb = take((plan.chunks + 2) / 2);
     return off;
 }
@@ -529,6 +538,7 @@ cudaError_t fused_propagate_launch(const RodParams& p, double* state, int64_t st
     a.rods = (int)p.rods;
     a.m = (int)p.m;
     a.chunks = plan.chunks;
+    a.chunk_fixed = plan.fixed;
     a.m_magic = 0xFFFFFFFFu / (unsigned)p.m + 1u;
     a.lj_on = (p.rods >= 2 && p.lj_well > 0.0) ? 1 : 0;  // propagators.cpp:70
     a.max_disp = 10.0 * p.ds;

@@ -27,6 +27,7 @@ struct MrsPlan {
     size_t counters = 0;
     int variant = 0;  // kernel variant forced by the plan (0 = mrs_targets_per_thread())
     int tail = 0;     // 0: equal chunks; c1 << 8 | m: chunks after the first c1 are 1/m size
+    int fixed = 0;    // > 0: chunks of exactly `fixed` sources, the last one takes the rest
 };
 constexpr int kMrsThreads = 256;  // targets per block (one or two per thread)
 
