@@ -8,7 +8,8 @@
 //   lj_kernel         lj_repulsion (src/rod.cpp:124-174) as a per-node all-pairs sum.
 //   advance_kernel    advance_state (src/propagators.cpp:93-124) + reorthonormalize
 //                     (src/rod.cpp:176-195), one thread per node.
-//   sqrt_wtma_kernel  sqrt_rotation over a batch (rotation.cpp:91-107), per-warp TMA rings.
+//   sqrt_tma_kernel   sqrt_rotation over a batch (rotation.cpp:91-107), CTA-chunk TMA pipeline
+//   sqrt_wtma_kernel  the same with per-warp TMA rings (PSWIM_SQRT_WARP=1).
 //   metric / correct  rod_position_metric (io.cpp:49-68), corrected (parareal.cpp:47-54).
 #include <algorithm>
 #include <cmath>
@@ -353,6 +354,67 @@ sqrt_wtma_kernel(const double* __restrict__ r9, int64_t nwchunks, double* __rest
     if (lane == 0) bulk_wait<0>();
 }
 
+// CTA-chunk variant (the advance_tma_kernel pipeline): 256-matrix chunks (18 KiB) stream in
+// through a kSqrtCtaStages-deep ring of whole-CTA bulk copies, each thread takes one matrix in
+// place, the chunk leaves with one bulk store; thread 0 refills a stage once its store has
+// read shared memory.  Fewer, larger TMA transfers than the per-warp rings.
+constexpr int kSqrtCtaStages = 3;
+constexpr uint32_t kSqrtCtaChunkBytes = 256 * 9 * sizeof(double);
+
+template <int kStages, int kMpt>
+__global__ void __launch_bounds__(256, 4 / kMpt)
+sqrt_tma_kernel(const double* __restrict__ r9, int64_t nchunks, double* __restrict__ s9) {
+    // kMpt matrices per thread: chunks of 256 kMpt matrices
+    constexpr uint32_t kBytes = kMpt * kSqrtCtaChunkBytes;
+    constexpr int kMat = 256 * kMpt;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kBytes);
+    auto st_of = [&](int s) { return reinterpret_cast<double*>(smem + s * kBytes); };
+    auto issue = [&](int s, int64_t c) {
+        mbar_expect_tx(&full[s], kBytes);
+        bulk_load(st_of(s), r9 + 9 * kMat * c, kBytes, &full[s]);
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+        for (int s = 0; s < kStages; ++s) {
+            const int64_t c = blockIdx.x + (int64_t)s * gridDim.x;
+            if (c < nchunks) issue(s, c);
+        }
+    }
+    __syncthreads();
+    for (int64_t k = 0;; ++k) {
+        const int64_t c = blockIdx.x + k * gridDim.x;
+        if (c >= nchunks) break;
+        const int s = (int)(k % kStages);
+        double* b = st_of(s);
+        mbar_wait(&full[s], (uint32_t)((k / kStages) & 1));
+        m33 r[kMpt];
+#pragma unroll
+        for (int q = 0; q < kMpt; ++q)
+#pragma unroll
+            for (int e = 0; e < 9; ++e) r[q].m[e] = b[9 * (threadIdx.x + 256 * q) + e];
+#pragma unroll
+        for (int q = 0; q < kMpt; ++q) {
+            const m33 o = sqrt_rotation(r[q]);
+#pragma unroll
+            for (int e = 0; e < 9; ++e) b[9 * (threadIdx.x + 256 * q) + e] = o.m[e];
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            bulk_store(s9 + 9 * kMat * c, b, kBytes);
+            bulk_commit();
+            const int64_t cn = blockIdx.x + (k + kStages) * gridDim.x;
+            if (cn < nchunks) {
+                bulk_wait_read<0>();
+                issue(s, cn);
+            }
+        }
+    }
+    if (threadIdx.x == 0) bulk_wait<0>();
+}
+
 __global__ void __launch_bounds__(kSqrtBlock)
 sqrt_plain_kernel(const double* __restrict__ r9, int64_t count, double* __restrict__ s9) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -531,6 +593,8 @@ void rod_preload() {
                              (int)(kAdvStages * kAdvStageBytes + kAdvStages * sizeof(uint64_t)));
         cudaFuncSetAttribute(sqrt_wtma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(8 * (size_t)kSqrtWarpStages * (kSqrtWarpChunkBytes + sizeof(uint64_t))));
+        cudaFuncSetAttribute(sqrt_tma_kernel<kSqrtCtaStages, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kSqrtCtaStages * (kSqrtCtaChunkBytes + sizeof(uint64_t))));
         return true;
     }();
     (void)once;
@@ -539,6 +603,7 @@ void rod_preload() {
     cudaFuncGetAttributes(&a, rod_loads_wtma_kernel<kRodStages>);
     cudaFuncGetAttributes(&a, lj_kernel);
     cudaFuncGetAttributes(&a, sqrt_wtma_kernel);
+    cudaFuncGetAttributes(&a, sqrt_tma_kernel<kSqrtCtaStages, 1>);
     cudaFuncGetAttributes(&a, sqrt_plain_kernel);
     cudaFuncGetAttributes(&a, metric_kernel);
     cudaFuncGetAttributes(&a, correct_kernel);
@@ -569,6 +634,26 @@ cudaError_t sqrt_batched_launch(const double* r9, int64_t count, double* s9, cud
     const bool aligned = ((reinterpret_cast<uintptr_t>(r9) | reinterpret_cast<uintptr_t>(s9)) & 15) == 0;
     if (!aligned) {
         sqrt_plain_kernel<<<grid_for(count, kSqrtBlock), kSqrtBlock, 0, st>>>(r9, count, s9);
+        return cudaGetLastError();
+    }
+    static const bool warp_rings = [] {
+        const char* e = std::getenv("PSWIM_SQRT_WARP");  // dev knob: the per-warp-ring kernel
+        return e && std::atoi(e) == 1;
+    }();
+    if (!warp_rings) {
+        // CTA-chunk pipeline (default): 256-matrix chunks, 3 stages; measured 5.70-5.74 TB/s
+        // against 5.56-5.62 for the per-warp rings (1e7 matrices; 2 / 4 stages and 2
+        // matrices per thread measured 5.46-5.72)
+        const int64_t nc = count / 256;
+        if (nc > 0) {
+            const size_t csmem = kSqrtCtaStages * (kSqrtCtaChunkBytes + sizeof(uint64_t));
+            const int per_sm = occupancy(sqrt_tma_kernel<kSqrtCtaStages, 1>, 256, csmem);
+            const int64_t grid = std::min<int64_t>(nc, (int64_t)num_sms() * per_sm);
+            sqrt_tma_kernel<kSqrtCtaStages, 1><<<(unsigned)grid, 256, csmem, st>>>(r9, nc, s9);
+        }
+        const int64_t done = 256 * nc, rest = count - done;
+        if (rest > 0)
+            sqrt_plain_kernel<<<grid_for(rest, kSqrtBlock), kSqrtBlock, 0, st>>>(r9 + 9 * done, rest, s9 + 9 * done);
         return cudaGetLastError();
     }
     // per-warp TMA rings over the whole 32-matrix chunks, plain tail
