@@ -62,7 +62,7 @@ def main():
         print(f"  /*{addr:05x}*/ {ins}")
 
     section("HBM-streaming kernels (rod.cu): cp.async.bulk rings")
-    for pat, name in ((r"sqrt_wtma", "sqrt_wtma_kernel (batched sqrt_rotation)"),
+    for pat, name in ((r"sqrt_tma_kernel", "sqrt_tma_kernel (batched sqrt_rotation, CTA-chunk pipeline)"),
                       (r"rod_loads_wtma", "rod_loads_wtma_kernel (internal + nodal loads)"),
                       (r"advance_tma", "advance_tma_kernel (advance_state + reorthonormalize)")):
         ls = sass_cost.kernel_sass(LIB, pat)
@@ -73,8 +73,8 @@ def main():
               f"MUFU.RSQ64H {hh['MUFU.RSQ64H']}, LDG {sum(v for k, v in hh.items() if k.startswith('LDG'))}, "
               f"STG {sum(v for k, v in hh.items() if k.startswith('STG'))}")
 
-    section("fused_kernel<16, 128> (flagellum cluster): velocity exchange and FP64 mix")
-    ls = sass_cost.kernel_sass(LIB, r"fused_kernelILi16ELi128")
+    section("fused_kernel<16, 128, no timer> (flagellum cluster): velocity exchange and FP64 mix")
+    ls = sass_cost.kernel_sass(LIB, r"fused_kernelILi16ELi128ELb0")
     hh = hist(ls)
     print(f"{len(ls)} instructions")
     print("exchange / sync: " + show_hist(hh, [k for k in sorted(hh) if k.startswith(("STAS", "ST.ASYNC", "SYNCS", "MAPA", "UCGABAR", "BAR", "MEMBAR", "FENCE", "CCTL"))]))
