@@ -59,15 +59,28 @@ struct FusedArgs {
 // pairs, 4 chunk reduction + DSMEM velocity push, 5 cluster barrier, 6 advance.
 template <bool kOn>
 struct PhaseClock {
+    // cycles accumulate in registers (the phase index is a constant at every inlined call
+    // site) and reach global memory once, at the end of the launch: a global read-modify-write
+    // per mark would put its load latency into the next phase's count
     unsigned long long* prof;
     long long t;
+    unsigned long long acc[kFusedPhases];
+    __device__ __forceinline__ PhaseClock(unsigned long long* p, long long t0) : prof(p), t(t0) {
+#pragma unroll
+        for (int i = 0; i < kFusedPhases; ++i) acc[i] = 0ull;
+    }
     __device__ __forceinline__ void mark(int phase) {
         if constexpr (kOn) {
-            if (prof) {
-                const long long c = clock64();
-                prof[phase] += (unsigned long long)(c - t);
-                t = c;
-            }
+            const long long c = clock64();
+            acc[phase] += (unsigned long long)(c - t);
+            t = c;
+        }
+    }
+    __device__ __forceinline__ void flush() {
+        if constexpr (kOn) {
+            if (prof)
+#pragma unroll
+                for (int i = 0; i < kFusedPhases; ++i) prof[i] += acc[i];
         }
     }
 };
@@ -99,14 +112,14 @@ __device__ __forceinline__ void strain_table(const FusedArgs& a, double* om, dou
 // advances them into a per-warp tile, computes segment (g, g+1) per lane and gets segment
 // g - 1 by one shuffle -- the layout of rod_loads_wtma_kernel.  LJ needs every advanced
 // position first, so LJ systems take the phased version.
-template <int CS, int KP, bool kProf>
+template <int CS, int KP, bool kLj, bool kProf>
 __device__ __forceinline__ void fused_front(const FusedArgs& a, double* sm, const double* src, const double* vadv, double h,
                                             double* dst, const double* om, double* om_next, double t_next, unsigned& fl,
                                             PhaseClock<kProf>& pc) {
     const int tid = threadIdx.x, bs = blockDim.x, N = a.n, m = a.m, nseg = a.rods * (m - 1);
     double* pos = sm + a.off_pos;
     double2* rec = reinterpret_cast<double2*>(sm + a.off_rec);
-    if (!a.lj_on) {
+    if constexpr (!kLj) {
         const int warp = tid >> 5, lane = tid & 31, nw = (N + kFrontNodes - 1) / kFrontNodes;
         if (warp >= nw) {
             // the warps without front nodes tabulate the next rhs's preferred strain meanwhile
@@ -155,57 +168,57 @@ __device__ __forceinline__ void fused_front(const FusedArgs& a, double* sm, cons
         }
         __syncthreads();
         pc.mark(0);
-        return;
-    }
-    // phased (LJ) version
-    if (vadv) {
-        for (int i = tid; i < N; i += bs)
-            fl |= advance_node(src + i, vadv + i, vadv + 3 * KP + i, h, a.max_disp, dst + i, KP, KP, KP);
+    } else {
+        // phased (LJ) version
+        if (vadv) {
+            for (int i = tid; i < N; i += bs)
+                fl |= advance_node(src + i, vadv + i, vadv + 3 * KP + i, h, a.max_disp, dst + i, KP, KP, KP);
+            __syncthreads();
+        }
+        const double* xs = vadv ? dst : src;
+        double* fo = sm + a.off_f;
+        double* no = sm + a.off_n;
+        double* seg = sm + a.off_seg;
+        double* ljf = sm + a.off_lj;
+        for (int s = tid; s < nseg; s += bs) {
+            const int r = s / (m - 1), k = s % (m - 1);
+            if (!rod_segment_om(a.rod, xs + m * r, k, om[k], seg + 6 * s, KP)) fl |= kFlagDegenerate;
+        }
+        for (int i = tid; i < N; i += bs) {
+            double fx = 0, fy = 0, fz = 0;
+            const double xi = xs[i], yi = xs[KP + i], zi = xs[2 * KP + i];
+            const int ri = i / m, ki = i - ri * m;
+            for (int rj = 0, j = 0; rj < a.lj.rods; ++rj)
+                for (int kj = 0; kj < m; ++kj, ++j)
+                    lj_pair(a.lj, ri, ki, rj, kj, xi - xs[j], yi - xs[KP + j], zi - xs[2 * KP + j], fx, fy, fz);
+            ljf[3 * i] = fx;
+            ljf[3 * i + 1] = fy;
+            ljf[3 * i + 2] = fz;
+        }
         __syncthreads();
+        for (int g = tid; g < N; g += bs) {
+            const int r = g / m, k = g % m;
+            d3 f, tq;
+            rod_node(a.rod, xs + m * r, seg + 6 * (m - 1) * r, k, f, tq, KP);
+            f = f + ld3(ljf + 3 * g) * a.rod.inv_ds;
+            st3s(pos + g, KP, ld3s(xs + g, KP));
+            st3(fo + 3 * g, f);
+            st3(no + 3 * g, tq);
+        }
+        __syncthreads();
+        strain_table(a, om_next, t_next);  // (this rhs's segment pass is done: barrier above)
+        // stage every source relative to node 0 (the single target block's origin in mrs.cu)
+        const double ox = pos[0], oy = pos[KP], oz = pos[2 * KP];
+        for (int j = tid; j < N; j += bs) {
+            double2 r[9];
+            const d3 pj = ld3s(pos + j, KP);
+            if (!mrs_stage(&pj.x, 0, fo, no, j, ox, oy, oz, a.mc.scale, r)) fl |= kFlagNonFinite;
+    #pragma unroll
+            for (int q = 0; q < 9; ++q) rec[q * KP + j] = r[q];
+        }
+        __syncthreads();
+        pc.mark(0);
     }
-    const double* xs = vadv ? dst : src;
-    double* fo = sm + a.off_f;
-    double* no = sm + a.off_n;
-    double* seg = sm + a.off_seg;
-    double* ljf = sm + a.off_lj;
-    for (int s = tid; s < nseg; s += bs) {
-        const int r = s / (m - 1), k = s % (m - 1);
-        if (!rod_segment_om(a.rod, xs + m * r, k, om[k], seg + 6 * s, KP)) fl |= kFlagDegenerate;
-    }
-    for (int i = tid; i < N; i += bs) {
-        double fx = 0, fy = 0, fz = 0;
-        const double xi = xs[i], yi = xs[KP + i], zi = xs[2 * KP + i];
-        const int ri = i / m, ki = i - ri * m;
-        for (int rj = 0, j = 0; rj < a.lj.rods; ++rj)
-            for (int kj = 0; kj < m; ++kj, ++j)
-                lj_pair(a.lj, ri, ki, rj, kj, xi - xs[j], yi - xs[KP + j], zi - xs[2 * KP + j], fx, fy, fz);
-        ljf[3 * i] = fx;
-        ljf[3 * i + 1] = fy;
-        ljf[3 * i + 2] = fz;
-    }
-    __syncthreads();
-    for (int g = tid; g < N; g += bs) {
-        const int r = g / m, k = g % m;
-        d3 f, tq;
-        rod_node(a.rod, xs + m * r, seg + 6 * (m - 1) * r, k, f, tq, KP);
-        f = f + ld3(ljf + 3 * g) * a.rod.inv_ds;
-        st3s(pos + g, KP, ld3s(xs + g, KP));
-        st3(fo + 3 * g, f);
-        st3(no + 3 * g, tq);
-    }
-    __syncthreads();
-    strain_table(a, om_next, t_next);  // (this rhs's segment pass is done: barrier above)
-    // stage every source relative to node 0 (the single target block's origin in mrs.cu)
-    const double ox = pos[0], oy = pos[KP], oz = pos[2 * KP];
-    for (int j = tid; j < N; j += bs) {
-        double2 r[9];
-        const d3 pj = ld3s(pos + j, KP);
-        if (!mrs_stage(&pj.x, 0, fo, no, j, ox, oy, oz, a.mc.scale, r)) fl |= kFlagNonFinite;
-#pragma unroll
-        for (int q = 0; q < 9; ++q) rec[q * KP + j] = r[q];
-    }
-    __syncthreads();
-    pc.mark(0);
 }
 
 // Back half of an rhs: the O(N^2) MRS of the staged sources into vel[6 n] = (u, w) per node.
@@ -299,7 +312,7 @@ __device__ __forceinline__ void fused_mrs(const FusedArgs& a, double* sm, double
     pc.mark(4);
 }
 
-template <int CS, int KP, bool kProf>
+template <int CS, int KP, bool kLj, bool kProf>
 __global__ void __launch_bounds__(kFusedThreads, 1)
 fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, double dt, int scheme,
              unsigned* __restrict__ flags) {
@@ -330,7 +343,7 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
     cluster_barrier<CS>();  // barriers initialised before any CTA pushes into them
     unsigned fl = 0;
     const int crank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
-    PhaseClock<kProf> pc{(kProf && tid == 0 && crank == 0) ? a.prof : nullptr, clock64()};
+    PhaseClock<kProf> pc((kProf && tid == 0 && crank == 0) ? a.prof : nullptr, kProf ? clock64() : 0);
     // One loop iteration per rhs (one call site of each phase: half the code of a per-step
     // body, which matters for the instruction cache).  Buffers are picked by shared-memory
     // offsets (no runtime-indexed local arrays, so every state access stays an LDS):
@@ -356,7 +369,7 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
         double* dst = sm + (mid ? a.off_xm : o_start);
         // strain tables: this rhs reads table p; the next rhs's (at t + dt/2 for the RK2
         // midpoint, else the next step's t; t += dt below) goes to table p ^ 1 meanwhile
-        fused_front<CS, KP, kProf>(a, sm, src, vadv, mid ? 0.5 * dt : dt, dst, sm + a.off_om + p * a.m,
+        fused_front<CS, KP, kLj, kProf>(a, sm, src, vadv, mid ? 0.5 * dt : dt, dst, sm + a.off_om + p * a.m,
                                    sm + a.off_om + (p ^ 1) * a.m, rk2 && !mid ? t + 0.5 * dt : t + dt, fl, pc);
         fused_mrs<CS, KP, kProf>(a, sm, sm + a.off_vel + p * 6 * KP, &vbar[p], pc, sp);
         if (!rk2 || mid) t += dt;  // propagators.cpp:159
@@ -377,34 +390,39 @@ fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, 
     if (crank == 0)
         for (int k = tid; k < 12 * N; k += bs) state[k] = out[(k % 12) * KP + k / 12];
     if (fl) atomicOr(flags, fl);
+    pc.flush();
     cluster_barrier<CS>();  // no CTA may exit while others still push partials into it
 }
 
 // Function attributes are set once per process, at context creation (fused_preload), never on
 // a launch path: a driver call that takes the context lock while a peer's device-side wait is
 // pending could otherwise stall another thread's launch (Parareal peer hand-offs).
-template <int CS, int KP, bool kProf>
+template <int CS, int KP, bool kLj, bool kProf>
 cudaError_t configure_one() {
-    cudaError_t e = cudaFuncSetAttribute(fused_kernel<CS, KP, kProf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(fused_kernel<CS, KP, kLj, kProf>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess && CS > 8)
-        e = cudaFuncSetAttribute(fused_kernel<CS, KP, kProf>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        e = cudaFuncSetAttribute(fused_kernel<CS, KP, kLj, kProf>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return e;
 }
 
 template <int CS, int KP>
 void load_cs() {
     cudaFuncAttributes fa;  // loads the module on the current device (lazy loading)
-    cudaFuncGetAttributes(&fa, fused_kernel<CS, KP, false>);
-    cudaFuncGetAttributes(&fa, fused_kernel<CS, KP, true>);
+    cudaFuncGetAttributes(&fa, fused_kernel<CS, KP, false, false>);
+    cudaFuncGetAttributes(&fa, fused_kernel<CS, KP, false, true>);
+    cudaFuncGetAttributes(&fa, fused_kernel<CS, KP, true, false>);
+    cudaFuncGetAttributes(&fa, fused_kernel<CS, KP, true, true>);
 }
 
 template <int CS, int KP>
 void configure_cs() {
-    configure_one<CS, KP, false>();
-    configure_one<CS, KP, true>();
+    configure_one<CS, KP, false, false>();
+    configure_one<CS, KP, false, true>();
+    configure_one<CS, KP, true, false>();
+    configure_one<CS, KP, true, true>();
 }
 
-template <int CS, int KP, bool kProf>
+template <int CS, int KP, bool kLj, bool kProf>
 cudaError_t launch_one(const FusedArgs& a, size_t smem, double* state, int64_t steps, double t0, double dt, int scheme,
                       unsigned* flags, cudaStream_t st) {
     // (function attributes: configure_cs, run by fused_preload at context creation)
@@ -420,7 +438,7 @@ cudaError_t launch_one(const FusedArgs& a, size_t smem, double* state, int64_t s
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, fused_kernel<CS, KP, kProf>, a, state, steps, t0, dt, scheme, flags);
+    return cudaLaunchKernelEx(&cfg, fused_kernel<CS, KP, kLj, kProf>, a, state, steps, t0, dt, scheme, flags);
 }
 
 // the phase-timer instantiation only for pswim_fused_profile: the production kernel has no
@@ -428,8 +446,14 @@ cudaError_t launch_one(const FusedArgs& a, size_t smem, double* state, int64_t s
 template <int CS, int KP>
 cudaError_t launch_cs(const FusedArgs& a, size_t smem, double* state, int64_t steps, double t0, double dt, int scheme,
                       unsigned* flags, cudaStream_t st) {
-    return a.prof ? launch_one<CS, KP, true>(a, smem, state, steps, t0, dt, scheme, flags, st)
-                  : launch_one<CS, KP, false>(a, smem, state, steps, t0, dt, scheme, flags, st);
+    // LJ systems take the phased front, the others the warp-tiled one: separate kernels, so
+    // neither carries the other's code (the flagellum kernel is 3.4k instead of 5.1k SASS
+    // instructions: +2.2 % from instruction-cache misses alone)
+    if (a.lj_on)
+        return a.prof ? launch_one<CS, KP, true, true>(a, smem, state, steps, t0, dt, scheme, flags, st)
+                      : launch_one<CS, KP, true, false>(a, smem, state, steps, t0, dt, scheme, flags, st);
+    return a.prof ? launch_one<CS, KP, false, true>(a, smem, state, steps, t0, dt, scheme, flags, st)
+                  : launch_one<CS, KP, false, false>(a, smem, state, steps, t0, dt, scheme, flags, st);
 }
 
 // Shared-memory layout of a fused launch (offsets in doubles, 16-B aligned) into a; returns the

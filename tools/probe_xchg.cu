@@ -1,6 +1,7 @@
 // probe_xchg.cu — dev microbenchmark (not part of the library): the fused kernel's per-rhs
 // velocity all-to-all on a 16-CTA cluster, 7 targets x 6 values per CTA (100-node flagellum):
 //   mode 0: one st.async per value per destination CTA (the fused kernel's push), 42 threads
+//   mode 2: one st.async.v2.f64 per value pair per destination CTA, 21 threads
 //   mode 1: one cp.async.bulk shared::cta -> shared::cluster per destination CTA (336 B,
 //           target-major [i][6] runs), issued by 16 threads after a named barrier
 // Cycles per exchange round at CTA 0 (push + wait for all 600 values), averaged.
@@ -60,6 +61,16 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(384, 1) xchg(double
                                  "d"(1.0 * r + tid), "r"(mapa(lb, rr))
                                  : "memory");
             }
+        } else if (MODE == 2) {
+            if (2 * tid < mine) {
+                const uint32_t la = su32(&buf[b][rank * per_cta + 2 * tid]), lb = su32(&bar[b]);
+#pragma unroll
+                for (unsigned rr = 0; rr < 16; ++rr)
+                    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+                                     mapa(la, rr)),
+                                 "d"(1.0 * r + tid), "d"(2.0 * r + tid), "r"(mapa(lb, rr))
+                                 : "memory");
+            }
         } else {
             if (tid < mine) stage[b][tid] = 1.0 * r + tid;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -84,16 +95,19 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(384, 1) xchg(double
 int main() {
     double* d;
     cudaMalloc(&d, 64);
-    double h[2];
+    double h[3];
+    cudaFuncSetAttribute(xchg<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(xchg<0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(xchg<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     for (int i = 0; i < 2; ++i) {
         xchg<0><<<16, 384>>>(d, 2000, 42, 600);
         xchg<1><<<16, 384>>>(d, 2000, 42, 600);
+        xchg<2><<<16, 384>>>(d, 2000, 42, 600);
     }
     printf("launch: %s\n", cudaGetErrorString(cudaGetLastError()));
-    cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-    printf("st.async per value: %.0f cycles/exchange\ncp.async.bulk per CTA: %.0f cycles/exchange\nerr %s\n", h[0], h[1],
+    cudaMemcpy(h, d, 24, cudaMemcpyDeviceToHost);
+    printf("st.async per value: %.0f cycles/exchange\ncp.async.bulk per CTA: %.0f cycles/exchange\n"
+           "st.async.v2 per value pair: %.0f cycles/exchange\nerr %s\n", h[0], h[1], h[2],
            cudaGetErrorString(cudaDeviceSynchronize()));
     return 0;
 }
