@@ -422,7 +422,7 @@ pswim_ctx* pswim_create(int device, const pswim_scenario* sc, int stream_priorit
             return nullptr;
         }
         if (ctx->rp.rods >= 2 && ctx->rp.lj_well > 0.0 && ctx->rs.total_nodes >= kLjCellsMinNodes) {
-            // cell-list workspace + one sort (loads the sort kernels, see preload_kernels)
+            // cell-list workspace (its kernels are loaded by preload_kernels)
             if (lj_cells_reserve(ctx->rs.total_nodes, &ctx->lj_work, ctx->stream) != cudaSuccess) {
                 delete ctx;
                 return nullptr;
