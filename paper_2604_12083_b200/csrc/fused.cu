@@ -49,7 +49,6 @@ struct FusedArgs {
     int off_bar;           // two mbarriers (velocity buffers)
     int off_om;            // preferred strain per segment index (m - 1), two tables: rhs r reads r & 1
     int off_cb;            // MRS chunk bounds (chunks + 1 ints)
-    int part_stride;  // unused (kept for layout clarity)
     unsigned long long* prof;  // kFusedPhases clock64 counters (CTA 0, thread 0), nullptr = off
 };
 
@@ -213,7 +212,7 @@ __device__ __forceinline__ void fused_front(const FusedArgs& a, double* sm, cons
             double2 r[9];
             const d3 pj = ld3s(pos + j, KP);
             if (!mrs_stage(&pj.x, 0, fo, no, j, ox, oy, oz, a.mc.scale, r)) fl |= kFlagNonFinite;
-    #pragma unroll
+#pragma unroll
             for (int q = 0; q < 9; ++q) rec[q * KP + j] = r[q];
         }
         __syncthreads();
@@ -475,7 +474,6 @@ int64_t fused_layout(const RodParams& p, const MrsPlan& plan, int cs, FusedArgs&
     a.off_rec = take(18 * kp);
     a.off_vel = take(12 * kp);
     a.off_part = take(plan.chunks * tpc * 6);
-    a.part_stride = 0;
     const int64_t shared = off;  // union: front tiles | f, n, lj, seg
     a.off_tile = take(((n + kFrontNodes - 1) / kFrontNodes) * 32 * 12);
     const int64_t after_tiles = off;
