@@ -26,7 +26,14 @@ namespace cg = cooperative_groups;
 namespace pswim {
 namespace {
 
-constexpr int kFusedThreads = 384;  // 12 warps (>= the 9 front warps at N = 256): 168 registers, no spills
+// Threads per CTA: 12 warps for KP = 256 (>= the 9 front warps at N = 256; 168 registers),
+// 8 warps for KP = 128 (N <= 128: <= 5 front warps).  Every phase loops over the CTA's
+// threads, so the count only sets the warps in flight; fewer idle warps make the per-rhs CTA
+// barriers cheaper (flagellum, 16 CTAs: 169.7k -> 172.9k RK2 steps/s at 256 threads).
+template <int KP>
+constexpr int fused_threads() {
+    return KP == 128 ? 256 : 384;
+}
 constexpr int kFrontNodes = 30;  // nodes owned per warp in the warp-tiled front pass
 // KP (template): plane stride of the shared-memory state, velocity, position and source-record
 // planes, 128 or 256 (>= n): a compile-time constant, so every strided access in the per-node
@@ -312,7 +319,7 @@ __device__ __forceinline__ void fused_mrs(const FusedArgs& a, double* sm, double
 }
 
 template <int CS, int KP, bool kLj, bool kProf>
-__global__ void __launch_bounds__(kFusedThreads, 1)
+__global__ void __launch_bounds__(fused_threads<KP>(), 1)
 fused_kernel(FusedArgs a, double* __restrict__ state, int64_t steps, double t0, double dt, int scheme,
              unsigned* __restrict__ flags) {
     extern __shared__ __align__(16) double sm[];
@@ -427,7 +434,7 @@ cudaError_t launch_one(const FusedArgs& a, size_t smem, double* state, int64_t s
     // (function attributes: configure_cs, run by fused_preload at context creation)
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(CS);
-    cfg.blockDim = dim3(kFusedThreads);
+    cfg.blockDim = dim3(fused_threads<KP>());
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
