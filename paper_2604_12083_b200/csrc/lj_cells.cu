@@ -300,7 +300,7 @@ namespace {
 // Workspace: key (bucket per node), cell_start (bucket sizes -> starts), cell_end (scatter
 // cursors -> ends), idx_sorted (nodes in bucket order), pos / rk (gathered), tmp (tile sums
 // and the scan's arrival counter).
-cudaError_t lj_grow(int64_t total, int H, LjWork* w) {
+cudaError_t lj_grow(int64_t total, int H, LjWork* w, cudaStream_t st) {
     cudaError_t e;
     if (w->cap_nodes < total || w->cap_buckets < H) {
         w->release();
@@ -313,7 +313,7 @@ cudaError_t lj_grow(int64_t total, int H, LjWork* w) {
             (e = cudaMalloc(&w->pos, sizeof(double) * 3 * n)) != cudaSuccess ||
             (e = cudaMalloc(&w->rk, sizeof(int2) * n)) != cudaSuccess ||
             (e = cudaMalloc(&w->tmp, tmp)) != cudaSuccess ||
-            (e = cudaMemset(w->tmp, 0, tmp)) != cudaSuccess)
+            (e = cudaMemsetAsync(w->tmp, 0, tmp, st)) != cudaSuccess)  // scan arrival counter
             return e;
         w->tmp_bytes = tmp;
         w->cap_nodes = total;
@@ -328,7 +328,7 @@ cudaError_t lj_cells_launch(const RodParams& p, const double* state, double* for
     if (total == 0) return cudaSuccess;
     const int n = (int)total;
     const int H = lj_buckets(total);  // power of two >= 1024: whole scan tiles
-    cudaError_t e = lj_grow(total, H, w);
+    cudaError_t e = lj_grow(total, H, w, st);
     if (e != cudaSuccess) return e;
     const double inv_h = 1.0 / p.lj_cutoff;
     const unsigned mask = (unsigned)H - 1u;
@@ -348,10 +348,10 @@ cudaError_t lj_cells_launch(const RodParams& p, const double* state, double* for
     return cudaGetLastError();
 }
 
-cudaError_t lj_cells_reserve(int64_t total, LjWork* w, cudaStream_t) {
+cudaError_t lj_cells_reserve(int64_t total, LjWork* w, cudaStream_t st) {
     // the workspace for `total` nodes, allocated at context creation (no allocation on the
     // rhs path)
-    return lj_grow(total, lj_buckets(total), w);
+    return lj_grow(total, lj_buckets(total), w, st);
 }
 
 void lj_cells_preload() {
