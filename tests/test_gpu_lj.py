@@ -90,3 +90,31 @@ def test_rhs_with_cell_list_lj_matches_oracle(gpu, oracle):
     scale = max(np.abs(ou).max(), np.abs(ow).max())
     assert max(np.abs(u - ou).max(), np.abs(w - ow).max()) <= 1e-10 * scale
     ctx.close()
+
+
+@pytest.mark.parametrize("squeeze", [0.02, 0.002])
+def test_cell_list_crowded_buckets(gpu, oracle, squeeze):
+    """Crowded cells: the suspension squeezed towards its centre so that buckets hold tens to
+    hundreds of nodes -- the per-bucket sort's warp network (<= 128 members) and its in-place
+    fallback (> 128) -- against the all-pairs kernel, the oracle, and a bitwise repeat."""
+    from paper_2604_12083_b200.device import Context
+
+    sc, x = _suspension(0.02)
+    xs = x.reshape(-1, 12)
+    c = xs[:, 0:3].mean(axis=0)
+    xs[:, 0:3] = c + squeeze * (xs[:, 0:3] - c)
+    x = xs.reshape(-1)
+    rc = 2.0 ** (1.0 / 6.0) * sc.lj_sigma
+    cell = np.floor(xs[:, 0:3] / rc).astype(np.int64)
+    _, counts = np.unique(cell, axis=0, return_counts=True)
+    assert counts.max() > (16 if squeeze > 0.01 else 128)
+    ctx = Context(0, sc)
+    cells = _forces(ctx, x, 2)
+    pairs = _forces(ctx, x, 1)
+    want = oracle.lj_repulsion(x, 40, 64, 0.01, sc.lj_sigma, sc.lj_self_exclusion)
+    scale = np.abs(want).max()
+    assert scale > 0
+    assert np.max(np.abs(cells - pairs)) <= 1e-12 * scale
+    assert np.max(np.abs(cells - want)) <= 1e-12 * scale
+    assert np.array_equal(_forces(ctx, x, 2), cells)
+    ctx.close()
