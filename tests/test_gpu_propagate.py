@@ -138,7 +138,10 @@ def test_quiet_rod_zero_rhs(gpu):
                                              (dict(rod_count=1, nodes_per_rod=21), 1, 40),
                                              (dict(rod_count=4, nodes_per_rod=21, placement=1, lj_well_depth=0.01,
                                                    seed=2), 1, 20),
-                                             (dict(rod_count=2, nodes_per_rod=128, epsilon=0.08), 1, 10)])
+                                             (dict(rod_count=2, nodes_per_rod=128, epsilon=0.08), 1, 10),
+                                             (dict(rod_count=3, nodes_per_rod=60, placement=1, lj_well_depth=0.01,
+                                                   seed=3), 0, 7),  # N = 180: 384 threads, LJ, Euler, odd
+                                             (dict(rod_count=1, nodes_per_rod=37), 1, 9)])  # 7 chunks, last short
 def test_fused_propagate_bitwise_equals_launched_path(gpu, oracle, kw, scheme, steps):
     """The fused cluster kernel (N <= 256) reproduces the per-step launched kernels bitwise
     and the oracle to 1e-10."""
