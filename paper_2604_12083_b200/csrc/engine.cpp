@@ -207,6 +207,12 @@ class GpuExec final : public Executor {
             const int prio = i < wave_lanes ? hi : lo;
             pswim_ctx* c = pooled_ctx(device, sc, prio);
             if (!c) throw CodeError(PSWIM_ECUDA, "parareal: cannot create lane context");
+            // Small systems (fused cluster kernel): the wavefront lanes (coarse sweep,
+            // correctors: the sequential critical path) take 16-CTA clusters while at most 8
+            // fine lanes run 8-CTA ones beside them (flagellum, n = 8: l = 1 823k -> 851k
+            // simulated steps/s; fine lanes on 16 CTAs no longer fit side by side: 631k).
+            // The cluster size only splits targets: results are bitwise unchanged.
+            if (i < wave_lanes && fine_lanes <= 8) pswim_set_fused(c, 16);
             lanes_.push_back(c);
             prios_.push_back(prio);
         }
@@ -224,7 +230,10 @@ class GpuExec final : public Executor {
         if (slab_) cudaFree(slab_);
         if (d_rows_) cudaFree(d_rows_);
         if (h_rows_) cudaFreeHost(h_rows_);
-        for (size_t i = 0; i < lanes_.size(); ++i) release_ctx(lanes_[i], prios_[i]);
+        for (size_t i = 0; i < lanes_.size(); ++i) {
+            pswim_set_fused(lanes_[i], 1);  // the pool's default cluster cap
+            release_ctx(lanes_[i], prios_[i]);
+        }
     }
     void reserve(int buffers) override {
         cudaSetDevice(device_);
