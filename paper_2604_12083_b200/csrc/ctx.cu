@@ -224,11 +224,22 @@ int pswim_ctx::propagate_async(const double* d_in, double t0, double t1, int sch
         return PSWIM_OK;
     }
     if (fused_on && !timing_on && fused_cluster_size(rp, fused_max_cs) > 0) {
-        // the whole interval in one launch, bitwise identical to the loop below
-        const cudaError_t e = fused_propagate_launch(rp, d_out, steps, t0, dt, scheme, d_flags, stream, nullptr,
-                                                     fused_max_cs);
-        if (e != cudaSuccess) return fail(PSWIM_ECUDA, std::string("fused_propagate: ") + cudaGetErrorString(e));
-        return PSWIM_OK;
+        // the whole interval in one launch, bitwise identical to the loop below.  A cluster the
+        // GPU cannot place (cudaErrorInvalidClusterSize: a partitioned GPU, too few SMs per
+        // GPC) is retried at half the size -- the cluster only splits the targets, so the
+        // result does not change -- down to 2 CTAs, then the launched path below.
+        int cap = fused_max_cs;
+        for (;;) {
+            const int cs = fused_cluster_size(rp, cap);
+            const cudaError_t e = fused_propagate_launch(rp, d_out, steps, t0, dt, scheme, d_flags, stream, nullptr,
+                                                         cap);
+            if (e == cudaSuccess) return PSWIM_OK;
+            if (e != cudaErrorInvalidClusterSize)
+                return fail(PSWIM_ECUDA, std::string("fused_propagate: ") + cudaGetErrorString(e));
+            cudaGetLastError();  // (a launch-configuration error is not sticky)
+            if (cs <= 2) break;
+            cap = cs / 2;
+        }
     }
     // graphs pay where kernel launches are a visible share of a step (mid-size systems); large
     // systems would only add the one-off capture to the first interval
