@@ -44,6 +44,9 @@ sys.path.insert(0, ROOT)
 # more hardware work queues than the default 8, so that the streams of one process (coarse,
 # fine, comm, engine lanes) do not serialise behind each other's device-side waits
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# every device / transport wait of the rank drivers completes in well under a minute in these
+# legs; a peer that died aborts the leg after 5 min instead of the library's 15 min default
+os.environ.setdefault("PSWIM_COMM_TIMEOUT_S", "300")
 
 N_POINTS = 16384
 EPS, MU = 0.1, 1.0
