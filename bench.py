@@ -567,7 +567,15 @@ def time_steps_leg(args, world, rank, local, dev):
     try:
         leg = parareal_sweep_leg(args, sc, x0, world, rank, local, dev, tr)
         try:
-            leg["space_parallel"] = space_parallel_leg(sc, x0, local, dev, tr, world)
+            sp = space_parallel_leg(sc, x0, local, dev, tr, world)
+            # strong scaling of the exact serial fine integration (no Parareal error) against the
+            # 1-GPU serial fine rate measured in the sweep leg
+            base = leg.get("serial_fine_steps_per_s")
+            if base:
+                sp["speedup_vs_1gpu_serial_fine"] = sp["value"] / base
+                if "value" in sp.get("fused_peer_allgather", {}):
+                    sp["fused_peer_allgather"]["speedup_vs_1gpu_serial_fine"] = sp["fused_peer_allgather"]["value"] / base
+            leg["space_parallel"] = sp
         except Exception as e:
             leg["space_parallel"] = {"error": f"{type(e).__name__}: {e}"}
         if world >= 4 and world % 2 == 0:
